@@ -1,0 +1,76 @@
+/*
+ * tcfft_b200.h - C ABI of the B200-native tcFFT (batched FP16 complex-to-complex
+ * forward FFT on sm_100a tensor cores).
+ *
+ * The entry points are the cuFFT-style plan/execute surface the tcFFT paper
+ * names and the reference package exposes in Python:
+ *
+ *   tcfftPlan1D   <- reference plan_1d(nx, batch)        pkg/src/tcfft/plan.py:116-122
+ *   tcfftPlan2D   <- reference plan_2d(nx, ny, batch)    pkg/src/tcfft/plan.py:125-138
+ *   tcfftExecC2C  <- reference execute(plan, data)       pkg/src/tcfft/executor.py:152-190
+ *   tcfftDestroy  <- (garbage collection of Plan)        pkg/src/tcfft/plan.py:57
+ *
+ * Data layout: interleaved fp16 (re, im) pairs (cuFFT CUDA_C_16F), i.e. the
+ * reference BatchedTensor pairs array (executor.py:25-51) in device memory,
+ * contiguous: 1D element j of sequence b at [b*nx + j]; 2D row-major (nx, ny)
+ * with ny contiguous.  The transform is forward (W = exp(-2*pi*i/N)),
+ * unnormalised, natural order in and out, and may run in place
+ * (odata == idata).  Errors map onto the reference's exception classes in the
+ * Python wrapper (UnsupportedSizeError, PlanArgumentError, ExecuteError).
+ * Plain pointers and sizes only: no framework types cross this boundary.
+ */
+#ifndef TCFFT_B200_H_
+#define TCFFT_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct tcfftPlanImpl* tcfftHandle;
+
+typedef enum tcfftResult_t {
+  TCFFT_SUCCESS = 0,
+  TCFFT_INVALID_PLAN = 1,  /* null / destroyed handle */
+  TCFFT_ALLOC_FAILED = 2,  /* device or host allocation failed */
+  TCFFT_INVALID_VALUE = 3, /* bad argument (batch < 1, null pointer, misaligned buffer) */
+  TCFFT_INVALID_SIZE = 4,  /* transform size not a power of two >= 2 */
+  TCFFT_EXEC_FAILED = 5,   /* kernel launch / CUDA runtime failure */
+  TCFFT_NOT_SUPPORTED = 6, /* valid size this build does not implement */
+  TCFFT_NO_DEVICE = 7      /* no sm_100 device available */
+} tcfftResult;
+
+/* Plan a batch of 1D transforms of length nx (reference plan.py:116). */
+tcfftResult tcfftPlan1D(tcfftHandle* plan, int nx, int batch);
+/* Plan a batch of 2D transforms over row-major (nx, ny) data (plan.py:125). */
+tcfftResult tcfftPlan2D(tcfftHandle* plan, int nx, int ny, int batch);
+/* Stream for subsequent executions (cudaStream_t passed as void*; NULL = legacy default). */
+tcfftResult tcfftSetStream(tcfftHandle plan, void* stream);
+/* Bytes of device workspace the plan owns (0 for single-pass plans). */
+tcfftResult tcfftGetWorkspaceSize(tcfftHandle plan, size_t* bytes);
+/* Forward FP16 C2C transform; idata/odata are device pointers to __half2
+ * (interleaved complex), 16-byte aligned; odata may equal idata. Asynchronous
+ * with respect to the host (stream-ordered). */
+tcfftResult tcfftExecC2C(tcfftHandle plan, const void* idata, void* odata);
+tcfftResult tcfftDestroy(tcfftHandle plan);
+
+const char* tcfftGetErrorString(tcfftResult r);
+int tcfftGetVersion(void);
+
+/* ---- introspection (host-only, no GPU needed) --------------------------
+ * tcfftDescribePlan writes a JSON description of the plan that tcfftPlan1D /
+ * tcfftPlan2D would build (passes, radices, chunking, smem/TMEM budget).
+ * tcfftPlanTables copies the per-pass host tables (row records, B matrices,
+ * twiddle tables) so CPU tests can emulate the kernel's dataflow exactly.
+ * Pass the null pointer to query the byte sizes. */
+tcfftResult tcfftDescribePlan(int dims, int nx, int ny, int batch, char* json, size_t cap);
+tcfftResult tcfftPlanTables(int dims, int nx, int ny, int batch, int pass, void* rows, size_t* rows_bytes,
+                            void* bmats, size_t* b_bytes, void* twid, size_t* t_bytes);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TCFFT_B200_H_ */

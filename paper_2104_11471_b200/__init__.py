@@ -1,0 +1,243 @@
+"""B200-native tcFFT: batched FP16 complex-to-complex forward FFT on sm_100a.
+
+Python host mirror of the reference package's plan/execute surface
+(reference ``pkg/src/tcfft/__init__.py:8-49``, ``plan.py``, ``executor.py``)
+over the C ABI in ``include/tcfft_b200.h``.  Data lives in torch CUDA tensors
+(interleaved fp16 pairs: ``torch.complex32`` or ``float16[..., 2]``); torch is
+only the device-memory / stream plumbing, every transform runs in the
+hand-written sm_100a kernels of ``libtcfft_b200.so``.
+
+    plan = plan_1d(4096, batch=16384)
+    execute(plan, x)            # in place, natural order, like the reference
+    y = execute(plan, x, out=y) # out of place
+"""
+
+from __future__ import annotations
+
+import ctypes
+import json
+import math
+from dataclasses import dataclass, field
+from functools import reduce
+
+from . import _lib
+
+__version__ = "0.1.0"
+
+KERNEL_CATALOG = tuple(2 ** k for k in range(1, 14))  # reference kernels.py:27
+VALID_CONT_SIZES = (4, 8, 16, 32, 64)                 # reference kernels.py:29
+MAX_KERNEL_RADIX = 8192                               # reference plan.py:18
+
+
+class UnsupportedSizeError(ValueError):
+    """Transform size is not a power of two >= 2 (reference plan.py:22)."""
+
+
+class PlanArgumentError(ValueError):
+    """Bad batch / continuous_size / precision (reference plan.py:26)."""
+
+
+class ExecuteError(ValueError):
+    """Data does not match the plan, or the device execution failed
+    (reference executor.py:21)."""
+
+
+def _check_pow2(n: int, what: str) -> None:
+    if not isinstance(n, int) or n < 2 or n & (n - 1):
+        raise UnsupportedSizeError(f"{what} must be a power of two >= 2, got {n}")
+
+
+def schedule_radices(n: int) -> tuple:
+    """The reference's greedy kernel schedule (plan.py:35-44), kept for plan
+    JSON / API compatibility.  The B200 pass decomposition is chosen
+    separately (``Plan.passes``); results need not be bit-identical across
+    schedules."""
+    _check_pow2(n, "transform length")
+    out, rem = [], n
+    while rem > MAX_KERNEL_RADIX:
+        out.append(MAX_KERNEL_RADIX)
+        rem //= MAX_KERNEL_RADIX
+    out.append(rem)
+    return tuple(out)
+
+
+def _validate_schedule(schedule, n: int) -> tuple:
+    schedule = tuple(int(r) for r in schedule)
+    for r in schedule:
+        if r not in KERNEL_CATALOG:
+            raise UnsupportedSizeError(f"radix {r} not in the kernel catalog")
+    if reduce(lambda a, b: a * b, schedule, 1) != n:
+        raise UnsupportedSizeError(f"schedule {schedule} does not multiply to {n}")
+    return schedule
+
+
+def _common_checks(batch, continuous_size, precision):
+    if not isinstance(batch, int) or batch < 1:
+        raise PlanArgumentError(f"batch must be >= 1, got {batch}")
+    if continuous_size not in VALID_CONT_SIZES:
+        raise PlanArgumentError(f"continuous_size must be one of {VALID_CONT_SIZES}")
+    if precision not in ("half", "double"):
+        raise PlanArgumentError("precision must be 'half' or 'double'")
+    if precision != "half":
+        raise PlanArgumentError("precision 'double' is a CPU reference mode; the B200 path computes in fp16 "
+                                "storage / fp32 accumulation only (no CPU fallback)")
+
+
+_STATUS_EXC = {
+    _lib.TCFFT_INVALID_SIZE: UnsupportedSizeError,
+    _lib.TCFFT_INVALID_VALUE: PlanArgumentError,
+    _lib.TCFFT_NOT_SUPPORTED: UnsupportedSizeError,
+}
+
+
+@dataclass(eq=False)
+class Plan:
+    """Immutable transform configuration (reference plan.py:57-102) owning a
+    device plan handle (twiddle tables, DFT matrices, launch geometry)."""
+
+    dims: int
+    nx: int
+    ny: int | None
+    batch: int
+    schedule_x: tuple
+    schedule_y: tuple | None
+    continuous_size: int = 32
+    precision: str = "half"
+    _handle: object = field(default=None, repr=False)
+    _desc: dict = field(default_factory=dict, repr=False)
+
+    @property
+    def n_logical(self) -> int:
+        return self.nx if self.dims == 1 else self.nx * self.ny
+
+    @property
+    def passes(self) -> list:
+        """B200 pass decomposition (one persistent kernel launch each)."""
+        return self._desc.get("passes", [])
+
+    def to_json(self) -> str:
+        return json.dumps({
+            "dims": self.dims, "nx": self.nx, "ny": self.ny, "batch": self.batch,
+            "schedule_x": list(self.schedule_x),
+            "schedule_y": list(self.schedule_y) if self.schedule_y else None,
+            "continuous_size": self.continuous_size, "precision": self.precision,
+        })
+
+    def describe(self) -> dict:
+        return dict(self._desc)
+
+    def destroy(self) -> None:
+        h = self._handle
+        if h is not None and h.value:
+            _lib.load().tcfftDestroy(h)
+            self._handle = None
+
+    def __del__(self):
+        try:
+            self.destroy()
+        except Exception:
+            pass
+
+
+def _create(dims, nx, ny, batch):
+    L = _lib.load()
+    h = ctypes.c_void_p()
+    st = L.tcfftPlan1D(ctypes.byref(h), nx, batch) if dims == 1 else L.tcfftPlan2D(ctypes.byref(h), nx, ny, batch)
+    if st != _lib.TCFFT_SUCCESS:
+        exc = _STATUS_EXC.get(st, ExecuteError)
+        raise exc(f"tcfftPlan{dims}D failed: {_lib.error_string(st)}")
+    return h
+
+
+def plan_1d(nx: int, batch: int, *, continuous_size: int = 32, precision: str = "half",
+            schedule=None) -> Plan:
+    """Plan a batch of 1D transforms of power-of-two length nx
+    (reference plan.py:116-122).  ``continuous_size`` and ``schedule`` are
+    validated as in the reference; the B200 kernels pick their own TMA box
+    widths and radix passes (results are invariant to both, reference
+    test_acceptance.py:128-138)."""
+    _check_pow2(nx, "nx")
+    _common_checks(batch, continuous_size, precision)
+    sched = schedule_radices(nx) if schedule is None else _validate_schedule(schedule, nx)
+    desc = _lib.describe(1, nx, 0, batch)
+    h = _create(1, nx, 0, batch)
+    return Plan(1, nx, None, batch, sched, None, continuous_size, precision, h, desc)
+
+
+def plan_2d(nx: int, ny: int, batch: int, *, continuous_size: int = 32, precision: str = "half") -> Plan:
+    """Plan batched 2D transforms over row-major (nx, ny) data: the contiguous
+    dimension (ny) first, then nx down the columns (reference plan.py:125-138)."""
+    _check_pow2(nx, "nx")
+    _check_pow2(ny, "ny")
+    _common_checks(batch, continuous_size, precision)
+    desc = _lib.describe(2, nx, ny, batch)
+    h = _create(2, nx, ny, batch)
+    return Plan(2, nx, ny, batch, schedule_radices(nx), schedule_radices(ny), continuous_size, precision, h, desc)
+
+
+def _as_pairs(t):
+    """View a torch complex32 / float16[..., 2] CUDA tensor as its interleaved
+    storage; returns (storage tensor, total complex elements)."""
+    import torch
+
+    if not isinstance(t, torch.Tensor):
+        raise ExecuteError(f"expected a torch CUDA tensor, got {type(t).__name__}")
+    if not t.is_cuda:
+        raise ExecuteError("data must be a CUDA tensor (the B200 path has no CPU fallback)")
+    if t.dtype == torch.complex32:
+        n = t.numel()
+    elif t.dtype == torch.float16:
+        if t.dim() == 0 or t.shape[-1] != 2:
+            raise ExecuteError(f"float16 data must have a trailing dimension of 2 (re, im), got {tuple(t.shape)}")
+        n = t.numel() // 2
+    else:
+        raise ExecuteError(f"plan precision half needs complex32 / float16 pair storage, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ExecuteError("data must be contiguous (interleaved pairs, batch-major)")
+    if t.data_ptr() % 16:
+        raise ExecuteError("data must be 16-byte aligned")
+    return t, n
+
+
+def execute(plan: Plan, data, out=None, stream=None):
+    """Run the planned forward transform (reference executor.py:152-190).
+
+    In place by default (returns ``data``); with ``out`` writes there and
+    returns ``out``.  Natural order in and out, unnormalised.  Asynchronous on
+    the current torch CUDA stream (or ``stream``)."""
+    import torch
+
+    if plan._handle is None:
+        raise ExecuteError("plan has been destroyed")
+    t, n = _as_pairs(data)
+    if n != plan.batch * plan.n_logical:
+        raise ExecuteError(f"data holds {n} complex elements, plan needs batch={plan.batch} x "
+                           f"len={plan.n_logical}")
+    if out is None:
+        o = t
+    else:
+        o, no = _as_pairs(out)
+        if no != n:
+            raise ExecuteError("out must hold as many elements as data")
+        if o.device != t.device:
+            raise ExecuteError("data and out must be on the same device")
+    L = _lib.load()
+    s = stream if stream is not None else torch.cuda.current_stream(t.device)
+    with torch.cuda.device(t.device):
+        st = L.tcfftSetStream(plan._handle, ctypes.c_void_p(s.cuda_stream))
+        if st == _lib.TCFFT_SUCCESS:
+            st = L.tcfftExecC2C(plan._handle, ctypes.c_void_p(t.data_ptr()), ctypes.c_void_p(o.data_ptr()))
+    if st != _lib.TCFFT_SUCCESS:
+        raise ExecuteError(f"tcfftExecC2C failed: {_lib.error_string(st)}")
+    return o if out is not None else data
+
+
+def flops_5nlogn(n_total: int, batch: int) -> float:
+    """Headline flop count of the project metric: 5 N log2 N per transform."""
+    return 5.0 * n_total * math.log2(n_total) * batch
+
+
+__all__ = [
+    "ExecuteError", "Plan", "PlanArgumentError", "UnsupportedSizeError", "execute", "flops_5nlogn",
+    "plan_1d", "plan_2d", "schedule_radices",
+]

@@ -1,0 +1,58 @@
+"""Build the sm_100a extension in-tree: paper_2104_11471_b200/libtcfft_b200.so.
+
+nvcc cross-compiles for sm_100a without a GPU.  ``-gencode
+arch=compute_100a,code=sm_100a`` is required: plain ``-arch=sm_100a`` also
+embeds compute_100 PTX, which ptxas rejects for tcgen05 instructions.
+"""
+
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+ROOT = PKG.parent
+CSRC = PKG / "csrc"
+LIB = PKG / "libtcfft_b200.so"
+SOURCES = [CSRC / "tcfft_api.cu", CSRC / "plan.cpp"]
+DEPS = SOURCES + [CSRC / "fft_kernel.cuh", CSRC / "sm100.cuh", CSRC / "plan.hpp", ROOT / "include" / "tcfft_b200.h"]
+
+
+def nvcc() -> str:
+    for c in (os.environ.get("NVCC"), "/usr/local/cuda/bin/nvcc", "nvcc"):
+        if c and (Path(c).exists() or c == "nvcc"):
+            return c
+    return "nvcc"
+
+
+def needs_build() -> bool:
+    if not LIB.exists():
+        return True
+    t = LIB.stat().st_mtime
+    return any(p.stat().st_mtime > t for p in DEPS)
+
+
+def build(force: bool = False, verbose: bool = False) -> Path:
+    if not force and not needs_build():
+        return LIB
+    cmd = [
+        nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
+        "-shared", "-Xcompiler", "-fPIC", "-cudart", "static", "-I", str(ROOT / "include"),
+        "-Xptxas", "-v" if verbose else "-O3",
+        "-o", str(LIB) + ".tmp", *map(str, SOURCES),
+    ]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        sys.stderr.write(res.stdout + res.stderr)
+        raise RuntimeError("nvcc failed building libtcfft_b200.so")
+    if verbose:
+        sys.stderr.write(res.stderr)
+    os.replace(str(LIB) + ".tmp", LIB)
+    return LIB
+
+
+if __name__ == "__main__":
+    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
+    print(LIB)

@@ -1,0 +1,416 @@
+// fft_kernel.cuh - one persistent sm_100a kernel per HBM pass of the batched
+// FP16 C2C FFT.
+//
+// Per CTA (128 threads; thread t <-> TMEM lane t <-> MMA row t):
+//   TMA tensor load of a chunk (E complex fp16 = 4E bytes, 128B-swizzled) ->
+//   stage 1 : each thread gathers the R_1 inputs of its butterfly(s) from the
+//             natural-order staging buffer (digit reversal folded into the
+//             addresses) and writes them to TMEM as the A operand;
+//             tcgen05.mma (A from TMEM, B = real 2R x 2R DFT block matrix in
+//             SMEM, D fp32 in TMEM)
+//   stage s>1: the previous epilogue wrote this stage's A operand into SMEM in
+//             the UMMA MN-major layout (split re/im planes, 16B vector stores);
+//             tcgen05.mma (A, B from SMEM)
+//   epilogue: tcgen05.ld the accumulator row, apply the NEXT stage's twiddle in
+//             fp32 (packed FFMA2; the per-row twiddle sequence c*w^j comes from
+//             a register recurrence, no table traffic), round once to fp16
+//             (cvt.rn.f16x2) and store the next operand, or (last stage) the
+//             natural-order output staging tile, which a TMA tensor store
+//             writes back to HBM.
+// HBM is touched exactly once per element per pass.  See DESIGN.md.
+#pragma once
+#include <cuda.h>
+#include <cstdint>
+#include <type_traits>
+#include "sm100.cuh"
+#include "plan.hpp"
+
+namespace tcfft {
+
+struct KParams {
+  int64_t chunks;
+  int32_t flat;            // 2: contiguous, rank-1 map; 1: contiguous, [total/W][W] map; 0: 3D column box
+  int32_t chunk_rows;      // flat: rows of the flat view per chunk (E / W)
+  int32_t strips_per_image;
+  int32_t C;               // box: columns per strip
+  int32_t gstride, ostride, swz;
+  int32_t tiles_max;
+  int32_t box_rows, n_sub;  // TMA sub-boxes per chunk (256-row limit)
+  int32_t sub_bytes;
+  const RowInfo* rows_tab;
+  const uint16_t* bblob;
+  int32_t bbytes;
+  int32_t smem_a, smem_b, smem_bar;
+};
+
+namespace dev {
+
+using namespace sm100;
+
+// ---------------------------------------------------------------- compile-time pass geometry
+template <int E_, int R1_, int R2_, int R3_, bool ROW_>
+struct Cfg {
+  static constexpr int E = E_;
+  static constexpr bool ROW = ROW_;
+  static constexpr int S = (R2_ == 0) ? 1 : ((R3_ == 0) ? 2 : 3);
+  static constexpr int N = R1_ * (R2_ ? R2_ : 1) * (R3_ ? R3_ : 1);
+  __host__ __device__ static constexpr int R(int s) { return s == 0 ? R1_ : (s == 1 ? R2_ : R3_); }
+  static constexpr int RL = R(S - 1);
+  __host__ __device__ static constexpr int KP(int s) { return 2 * R(s) < 16 ? 16 : 2 * R(s); }
+  __host__ __device__ static constexpr int NP(int s) { return KP(s); }
+  __host__ __device__ static constexpr int T(int s) { return E / (128 * R(s)); }
+  __host__ __device__ static constexpr int SBO(int s) { return 32 * R(s) + 16; }  // padded: consecutive 8-row groups hit distinct banks
+  __host__ __device__ static constexpr int TILEB(int s) { return 16 * SBO(s); }
+  __host__ __device__ static constexpr int BOFF(int s) { return s == 0 ? 0 : BOFF(s - 1) + KP(s - 1) * NP(s - 1) * 2; }
+  __host__ __device__ static constexpr int HSTEP(int s) { return (128 / R(s)) * SBO(s + 1); }
+  __host__ __device__ static constexpr int IMOFF(int s) { return 16 * R(s + 1); }
+  __host__ __device__ static constexpr int tmax(int a, int b) { return a > b ? a : b; }
+  static constexpr int TMAX = tmax(T(0), tmax(T(S > 1 ? 1 : 0), T(S - 1)));
+  // staging strides (words) and swizzle, compile-time for contiguous row passes
+  static constexpr int GS = N / R(0);
+  static constexpr int OS = N / RL;
+  static constexpr uint32_t SWZ = (N >= 32) ? 0x70u : 0u;
+  static constexpr bool AFF_IN = ROW && (SWZ == 0 || (GS * 4) % 1024 == 0);
+  static constexpr bool AFF_OUT = ROW && (SWZ == 0 || (OS * 4) % 1024 == 0);
+  // TMEM: D region (max over stages) then the stage-1 A region
+  __host__ __device__ static constexpr int DC(int s) { return T(s) * NP(s); }
+  static constexpr int DCOLS = tmax(DC(0), tmax(DC(S > 1 ? 1 : 0), DC(S - 1)));
+  static constexpr int ACOLS = T(0) * KP(0) / 2;
+  static constexpr int NEED = DCOLS + ACOLS;
+  static constexpr uint32_t COLS = NEED <= 32 ? 32 : NEED <= 64 ? 64 : NEED <= 128 ? 128 : NEED <= 256 ? 256 : 512;
+  static_assert(NEED <= 512, "TMEM budget");
+};
+
+DEVI uint32_t swz(uint32_t byte, uint32_t mask) { return byte ^ ((byte >> 3) & mask); }
+
+DEVI void sts128(uint32_t a, uint32_t x, uint32_t y, uint32_t z, uint32_t w) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(x), "r"(y), "r"(z), "r"(w) : "memory");
+}
+DEVI void sts32(uint32_t a, uint32_t x) { asm volatile("st.shared.b32 [%0], %1;" ::"r"(a), "r"(x) : "memory"); }
+DEVI uint32_t lds32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+  return v;
+}
+
+// Load NP fp32 accumulator columns of this thread's row.
+template <int NP>
+DEVI void load_acc(uint32_t taddr, float* x) {
+  uint32_t* r = reinterpret_cast<uint32_t*>(x);
+  if constexpr (NP == 16) {
+    tmem_ld16(taddr, r);
+  } else if constexpr (NP == 32) {
+    tmem_ld32(taddr, *reinterpret_cast<uint32_t(*)[32]>(r));
+  } else {
+    static_assert(NP == 64, "NP");
+    tmem_ld32(taddr, *reinterpret_cast<uint32_t(*)[32]>(r));
+    tmem_ld32(taddr + 32, *reinterpret_cast<uint32_t(*)[32]>(r + 32));
+  }
+  tmem_wait_ld();
+}
+
+DEVI float2 neg2(float2 a) { return make_float2(-a.x, -a.y); }  // folded into FFMA2 operand negation
+
+// Stage 1: gather R inputs (natural order) into TMEM A (interleaved re/im K order).
+template <class C>
+DEVI void gather_to_tmem(uint32_t s_in, int gbase, int gstride, uint32_t swzmask, uint32_t taddr) {
+  constexpr int R = C::R(0);
+  constexpr int KC = C::KP(0) / 2;  // TMEM columns (2 fp16 per column)
+  uint32_t v[KC];
+  if constexpr (C::AFF_IN) {
+    const uint32_t b0 = s_in + swz((uint32_t)gbase * 4u, C::SWZ);
+#pragma unroll
+    for (int m = 0; m < KC; ++m) v[m] = (m < R) ? lds32(b0 + m * C::GS * 4) : 0u;
+  } else {
+    const int gs = C::ROW ? C::GS : gstride;
+    const uint32_t msk = C::ROW ? C::SWZ : swzmask;
+#pragma unroll
+    for (int m = 0; m < KC; ++m)
+      v[m] = (m < R) ? lds32(s_in + swz((uint32_t)(gbase + m * gs) * 4u, msk)) : 0u;
+  }
+  if constexpr (KC == 8) {
+    tmem_st8(taddr, v);
+  } else if constexpr (KC == 16) {
+    tmem_st16(taddr, v);
+  } else {
+    static_assert(KC == 32, "KC");
+    tmem_st16(taddr, v);
+    tmem_st16(taddr + 16, v + 16);
+  }
+}
+
+// Accumulator row of stage s, outputs [j0, j0 + G): re -> xr[], im -> xi[].
+// D columns are planar: re_j at column j, im_j at column R + j.
+template <int R, int G>
+DEVI void load_group(uint32_t taddr, int j0, float* xr, float* xi) {
+  if constexpr (R <= 8) {
+    uint32_t r[16];
+    tmem_ld16(taddr, r);  // NP = 16: re 0..R-1, im R..2R-1
+    tmem_wait_ld();
+#pragma unroll
+    for (int j = 0; j < G; ++j) {
+      xr[j] = __uint_as_float(r[j]);
+      xi[j] = __uint_as_float(r[R + j]);
+    }
+  } else {
+    static_assert(G == 16, "G");
+    tmem_ld16(taddr + j0, reinterpret_cast<uint32_t*>(xr));
+    tmem_ld16(taddr + R + j0, reinterpret_cast<uint32_t*>(xi));
+    tmem_wait_ld();
+  }
+}
+
+// Writer epilogue of stage s: y_j = x_j * c * w^j (fp32, packed pairs),
+// rounded once to fp16 split planes, 16B stores into stage s+1's MN-major A.
+// Processed in groups of (up to) 16 outputs to bound register pressure.
+template <class C, int s>
+DEVI void writer_epilogue(uint32_t taddr, uint32_t dst, float2 c, float2 w) {
+  constexpr int R = C::R(s);
+  constexpr int G = R < 16 ? R : 16;
+  // pair (v_j, v_{j+1}) = (c w^j, c w^{j+1}); step w^2
+  const float2 w2 = make_float2(w.x * w.x - w.y * w.y, 2.f * w.x * w.y);
+  const float2 w2r = make_float2(w2.x, w2.x), w2i = make_float2(w2.y, w2.y);
+  float2 tr = make_float2(c.x, c.x * w.x - c.y * w.y);
+  float2 ti = make_float2(c.y, c.x * w.y + c.y * w.x);
+#pragma unroll
+  for (int g = 0; g < R / G; ++g) {
+    float xr[G], xi[G];
+    load_group<R, G>(taddr, g * G, xr, xi);
+#pragma unroll
+    for (int h = 0; h < G / 8; ++h) {
+      uint32_t pr[4], pi[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int j = 8 * h + 2 * q;
+        const float2 a = make_float2(xr[j], xr[j + 1]);
+        const float2 b = make_float2(xi[j], xi[j + 1]);
+        const float2 yr = ffma2(neg2(b), ti, fmul2(a, tr));  // xr*tr - xi*ti
+        const float2 yi = ffma2(b, tr, fmul2(a, ti));        // xr*ti + xi*tr
+        pr[q] = pack_half2(yr.x, yr.y);
+        pi[q] = pack_half2(yi.x, yi.y);
+        const float2 ntr = ffma2(neg2(ti), w2i, fmul2(tr, w2r));
+        const float2 nti = ffma2(ti, w2r, fmul2(tr, w2i));
+        tr = ntr;
+        ti = nti;
+      }
+      const uint32_t d = dst + ((g * G) / 8 + h) * C::HSTEP(s);
+      sts128(d, pr[0], pr[1], pr[2], pr[3]);
+      sts128(d + C::IMOFF(s), pi[0], pi[1], pi[2], pi[3]);
+    }
+  }
+}
+
+// Final epilogue: natural-order interleaved output into the staging tile.
+template <class C>
+DEVI void final_epilogue(uint32_t taddr, uint32_t s_out, int obase, int ostride, uint32_t swzmask) {
+  constexpr int R = C::RL;
+  constexpr int G = R < 16 ? R : 16;
+  const int os = C::ROW ? C::OS : ostride;
+  const uint32_t msk = C::ROW ? C::SWZ : swzmask;
+  const uint32_t b0 = s_out + swz((uint32_t)obase * 4u, C::SWZ);
+#pragma unroll
+  for (int g = 0; g < R / G; ++g) {
+    float xr[G], xi[G];
+    load_group<R, G>(taddr, g * G, xr, xi);
+#pragma unroll
+    for (int jj = 0; jj < G; ++jj) {
+      const int j = g * G + jj;
+      const uint32_t wv = pack_half2(xr[jj], xi[jj]);
+      if constexpr (C::AFF_OUT)
+        sts32(b0 + j * C::OS * 4, wv);
+      else
+        sts32(s_out + swz((uint32_t)(obase + j * os) * 4u, msk), wv);
+    }
+  }
+}
+
+DEVI void issue_load(const CUtensorMap* tm, const KParams& p, int64_t chunk, uint8_t* dst, uint64_t* bar) {
+  mbar_arrive_expect_tx(bar, (uint32_t)(p.n_sub * p.sub_bytes));
+  if (p.flat == 2) {
+    int32_t e0 = (int32_t)(chunk * p.chunk_rows);
+    for (int i = 0; i < p.n_sub; ++i) tma_load_1d(dst + i * p.sub_bytes, tm, e0 + i * p.box_rows, bar);
+  } else if (p.flat) {
+    int32_t row0 = (int32_t)(chunk * p.chunk_rows);
+    for (int i = 0; i < p.n_sub; ++i) tma_load_2d(dst + i * p.sub_bytes, tm, 0, row0 + i * p.box_rows, bar);
+  } else {
+    int32_t img = (int32_t)(chunk / p.strips_per_image);
+    int32_t cb = (int32_t)(chunk % p.strips_per_image);
+    for (int i = 0; i < p.n_sub; ++i) {
+      asm volatile(
+          "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
+          "%4}], [%5];" ::"r"(smem_u32(dst + i * p.sub_bytes)),
+          "l"(tm), "r"(cb * p.C), "r"(i * p.box_rows), "r"(img), "r"(smem_u32(bar))
+          : "memory");
+    }
+  }
+}
+
+DEVI void issue_store(const CUtensorMap* tm, const KParams& p, int64_t chunk, const uint8_t* src) {
+  if (p.flat == 2) {
+    int32_t e0 = (int32_t)(chunk * p.chunk_rows);
+    for (int i = 0; i < p.n_sub; ++i) tma_store_1d(tm, e0 + i * p.box_rows, src + i * p.sub_bytes);
+  } else if (p.flat) {
+    int32_t row0 = (int32_t)(chunk * p.chunk_rows);
+    for (int i = 0; i < p.n_sub; ++i) tma_store_2d(tm, 0, row0 + i * p.box_rows, src + i * p.sub_bytes);
+  } else {
+    int32_t img = (int32_t)(chunk / p.strips_per_image);
+    int32_t cb = (int32_t)(chunk % p.strips_per_image);
+    for (int i = 0; i < p.n_sub; ++i) {
+      asm volatile(
+          "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(tm),
+          "r"(cb * p.C), "r"(i * p.box_rows), "r"(img), "r"(smem_u32(src + i * p.sub_bytes))
+          : "memory");
+    }
+  }
+  bulk_commit();
+}
+
+// Issue the MMAs of stage s (one elected thread).
+template <class C, int s>
+DEVI void issue_stage_mma(uint32_t s_a, uint32_t s_b, uint32_t tD, uint32_t tA) {
+  constexpr int KP = C::KP(s), NP = C::NP(s), T = C::T(s);
+  if constexpr (s == 0) {
+    constexpr uint32_t idesc = make_idesc_f16(128, NP, 0, 0);  // A (TMEM) K-major, B K-major
+#pragma unroll
+    for (int t = 0; t < T; ++t)
+#pragma unroll
+      for (int q = 0; q < KP / 16; ++q)
+        mma_ts(tD + t * NP, tA + t * (KP / 2) + q * 8, make_sdesc(s_b + C::BOFF(s) + q * 32 * NP, 128, 256), idesc,
+               q > 0);
+  } else {
+    constexpr uint32_t idesc = make_idesc_f16(128, NP, 1, 0);  // A MN-major (split planes), B K-major
+#pragma unroll
+    for (int t = 0; t < T; ++t)
+#pragma unroll
+      for (int q = 0; q < KP / 16; ++q)
+        mma_ss(tD + t * NP, make_sdesc(s_a + t * C::TILEB(s) + q * 256, 128, C::SBO(s)),
+               make_sdesc(s_b + C::BOFF(s) + q * 32 * NP, 128, 256), idesc, q > 0);
+  }
+}
+
+}  // namespace dev
+
+template <int E, int R1, int R2, int R3, int MINB, bool ROW>
+__global__ void __launch_bounds__(128, MINB)
+    fft_pass_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ CUtensorMap tm_out,
+                    const KParams p) {
+  using namespace dev;
+  using C = Cfg<E, R1, R2, R3, ROW>;
+  constexpr int S = C::S;
+  constexpr int TM = C::TMAX;
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* s_in = smem;
+  uint8_t* s_a = smem + p.smem_a;
+  uint8_t* s_b = smem + p.smem_b;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.smem_bar);
+  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(bars + 2);
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const uint32_t s_in_u = smem_u32(s_in), s_a_u = smem_u32(s_a), s_b_u = smem_u32(s_b);
+
+  // constants: B matrices, once per CTA
+  for (int i = tid; i < p.bbytes / 16; i += 128)
+    reinterpret_cast<uint4*>(s_b)[i] = reinterpret_cast<const uint4*>(p.bblob)[i];
+  if (warp == 0) tmem_alloc<C::COLS>(s_tmem);
+  if (tid == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    fence_mbar_init();
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_in) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_out) : "memory");
+  }
+
+  // per-thread row records (host-built, see plan.cpp)
+  auto rec = [&](int s, int t) -> const RowInfo& { return p.rows_tab[((size_t)s * p.tiles_max + t) * 128 + tid]; };
+  // stage-0 writers have c = 1; the final stage needs only its output address
+  int gb[C::T(0)];
+  int waddr[S][TM];
+  float2 wc[S][TM], ww[S][TM];
+#pragma unroll
+  for (int t = 0; t < C::T(0); ++t) gb[t] = rec(0, t).gbase;
+#pragma unroll
+  for (int s = 0; s < S; ++s)
+#pragma unroll
+    for (int t = 0; t < TM; ++t) {
+      if (t < C::T(s)) {
+        const RowInfo& r = rec(s, t);
+        waddr[s][t] = r.addr;
+        if (s + 1 < S) ww[s][t] = make_float2(r.wr, r.wi);
+        if (s >= 1 && s + 1 < S) wc[s][t] = make_float2(r.cr, r.ci);
+      }
+    }
+
+  fence_proxy_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *s_tmem;
+  const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
+  const uint32_t tD = tbase;
+  const uint32_t tA = tbase + (uint32_t)C::DCOLS;
+
+  int64_t chunk = blockIdx.x;
+  if (tid == 0 && chunk < p.chunks) issue_load(&tm_in, p, chunk, s_in, &bars[0]);
+  uint32_t ld_phase = 0, mma_phase = 0;
+
+  for (; chunk < p.chunks; chunk += gridDim.x) {
+    mbar_wait(&bars[0], ld_phase);
+    ld_phase ^= 1;
+    // ---------------- stage 1: gather -> TMEM A
+#pragma unroll
+    for (int t = 0; t < C::T(0); ++t)
+      gather_to_tmem<C>(s_in_u, gb[t], p.gstride, (uint32_t)p.swz, tA + lane_off + t * (C::KP(0) / 2));
+    tmem_wait_st();
+    tc_fence_before();
+    __syncthreads();
+    if (tid == 0) {
+      tc_fence_after();
+      int64_t nxt = chunk + gridDim.x;
+      if (nxt < p.chunks) issue_load(&tm_in, p, nxt, s_in, &bars[0]);  // staging buffer is free again
+      bulk_wait_read0();  // previous chunk's output store no longer reads s_a
+      issue_stage_mma<C, 0>(s_a_u, s_b_u, tD, tA);
+      mma_commit(&bars[1]);
+    }
+    mbar_wait(&bars[1], mma_phase);
+    mma_phase ^= 1;
+    tc_fence_after();
+
+    // ---------------- stages 2..S
+    auto writer = [&](auto sc) {
+      constexpr int s = decltype(sc)::value;
+#pragma unroll
+      for (int t = 0; t < C::T(s); ++t)
+        writer_epilogue<C, s>(tD + lane_off + t * C::NP(s), s_a_u + waddr[s][t],
+                              s == 0 ? make_float2(1.f, 0.f) : wc[s][t], ww[s][t]);
+      fence_proxy_async_smem();
+      tc_fence_before();
+      __syncthreads();
+      if (tid == 0) {
+        tc_fence_after();
+        issue_stage_mma<C, s + 1>(s_a_u, s_b_u, tD, tA);
+        mma_commit(&bars[1]);
+      }
+      mbar_wait(&bars[1], mma_phase);
+      mma_phase ^= 1;
+      tc_fence_after();
+    };
+    if constexpr (S >= 2) writer(std::integral_constant<int, 0>{});
+    if constexpr (S >= 3) writer(std::integral_constant<int, 1>{});
+    // ---------------- final epilogue -> output staging (reuses s_a)
+#pragma unroll
+    for (int t = 0; t < C::T(S - 1); ++t)
+      final_epilogue<C>(tD + lane_off + t * C::NP(S - 1), s_a_u, waddr[S - 1][t], p.ostride, (uint32_t)p.swz);
+    fence_proxy_async_smem();
+    tc_fence_before();
+    __syncthreads();
+    if (tid == 0) issue_store(&tm_out, p, chunk, s_a);
+  }
+  if (tid == 0) bulk_wait0();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 0) tmem_dealloc<C::COLS>(tbase);
+}
+
+}  // namespace tcfft

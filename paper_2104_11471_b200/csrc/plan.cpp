@@ -1,0 +1,378 @@
+// plan.cpp - host-side planner (see plan.hpp).  Pure C++, no CUDA calls, so the
+// same tables can be built and checked on a CPU-only machine.
+//
+// Algorithm (reference pkg/src/tcfft/kernels.py:323-356, plan.py:141-158): the
+// transform is N = R_1 * R_2 * ... * R_S.  Stage s combines R_s sub-spectra of
+// length n2_s = R_1..R_{s-1}.  With the reference's digit-reversed positions
+// p = k + n2*m + n2*R*blk, stage s butterfly (k, blk) reads input m = d_s and
+// writes output j; its input m carries twiddle W_{R n2}^{m k}.  Stage 1 reads
+// natural-order input x[m*N/R_1 + b] directly (digit reversal folded into the
+// gather addresses); the last stage writes X[k + (N/R_S) j] in natural order.
+#include "plan.hpp"
+
+#include <cmath>
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <tuple>
+
+namespace tcfft {
+
+namespace {
+
+uint16_t f64_to_f16_rne(double x) {
+  // IEEE binary16, round to nearest even, with subnormals and overflow to inf.
+  uint16_t sign = std::signbit(x) ? 0x8000 : 0;
+  double a = std::fabs(x);
+  if (std::isnan(x)) return 0x7e00;
+  if (a >= 65520.0) return sign | 0x7c00;
+  if (a < std::ldexp(1.0, -25)) {
+    // below half the smallest subnormal (ties at exactly 2^-25 round to even 0)
+    return sign;
+  }
+  int e;
+  double m = std::frexp(a, &e);  // a = m * 2^e, m in [0.5, 1)
+  int exp16 = e - 1 + 15;        // biased exponent for 1.xxx * 2^(e-1)
+  if (exp16 <= 0) {
+    // subnormal: value = q * 2^-24
+    double q = a * std::ldexp(1.0, 24);
+    double r = std::nearbyint(q);  // default rounding mode: nearest-even
+    return sign | (uint16_t)r;
+  }
+  double frac = (m * 2.0 - 1.0) * 1024.0;  // 10-bit mantissa, fractional
+  double r = std::nearbyint(frac);
+  uint32_t mant = (uint32_t)r;
+  if (mant == 1024) {
+    mant = 0;
+    exp16 += 1;
+    if (exp16 >= 31) return sign | 0x7c00;
+  }
+  return sign | (uint16_t)(exp16 << 10) | (uint16_t)mant;
+}
+
+double f16_to_f64(uint16_t h) {
+  int s = h >> 15, e = (h >> 10) & 31, m = h & 1023;
+  double v;
+  if (e == 0)
+    v = std::ldexp((double)m, -24);
+  else if (e == 31)
+    v = m ? NAN : INFINITY;
+  else
+    v = std::ldexp(1.0 + m / 1024.0, e - 15);
+  return s ? -v : v;
+}
+
+// W_n^e = exp(-2 pi i e / n) with the exponent reduced exactly first
+// (reference twiddle.py:21-42).
+void root(int64_t e, int64_t n, double* re, double* im) {
+  int64_t r = ((e % n) + n) % n;
+  double ang = -2.0 * M_PI * (double)r / (double)n;
+  *re = std::cos(ang);
+  *im = std::sin(ang);
+}
+
+struct Bf {
+  int32_t tr, k, blk;
+};
+
+}  // namespace
+
+std::vector<int> choose_radices(int n) {
+  switch (n) {
+    case 2: return {2};
+    case 4: return {4};
+    case 8: return {8};
+    case 16: return {16};
+    case 32: return {32};
+    case 64: return {8, 8};
+    case 128: return {16, 8};
+    case 256: return {16, 16};
+    case 512: return {16, 32};
+    case 1024: return {32, 32};
+    case 2048: return {16, 16, 8};
+    case 4096: return {16, 16, 16};
+    case 8192: return {16, 16, 32};
+    case 16384: return {16, 32, 32};
+    default: return {};
+  }
+}
+
+int chunk_elems_for(int n) {
+  if (n <= 2) return 1024;
+  if (n == 4) return 2048;
+  if (n <= 4096) return 4096;
+  return n;  // 8192, 16384: one transform per chunk
+}
+
+bool build_pass(PassPlan& p, int kind, int N, int64_t count, int64_t images, int cols, std::string* err) {
+  std::vector<int> rad = choose_radices(N);
+  if (rad.empty()) {
+    if (err) *err = "no single-pass radix schedule for N=" + std::to_string(N);
+    return false;
+  }
+  p = PassPlan();
+  p.kind = kind;
+  p.N = N;
+  p.S = (int)rad.size();
+  if (kind == kPassRow) {
+    p.E = chunk_elems_for(N);
+    p.T = p.E / N;
+    p.count = count;
+    p.chunks = (count + p.T - 1) / p.T;
+  } else {
+    // Column strips of an images x N x cols array: C columns of IMG images per
+    // chunk, E = N * C * IMG = max(chunk_elems_for(N), 4 N) (C >= 4: >= 16 B runs).
+    p.E = std::max(chunk_elems_for(N), 4 * N);
+    int ci = p.E / N;  // C * IMG
+    if (ci <= cols) {
+      p.C = ci;
+      p.IMG = 1;
+    } else {
+      p.C = cols;
+      p.IMG = ci / cols;
+    }
+    if (p.C < cols && p.C > 256) {
+      if (err) *err = "unsupported 2D column strip geometry";
+      return false;
+    }
+    p.T = p.C * p.IMG;
+    p.images = images;
+    p.rows = N;
+    p.cols = cols;
+    p.count = images * (int64_t)cols;
+    p.chunks = (images + p.IMG - 1) / p.IMG * (int64_t)(cols / p.C);
+  }
+  const int E = p.E, T = p.T, S = p.S;
+  const int C = p.C, NN = N;
+  if (E < 128 * rad[0] || E > 16384) {
+    if (err) *err = "unsupported chunk size";
+    return false;
+  }
+  const bool row = kind == kPassRow;
+  auto w_addr = [&](int tr, int n) -> int32_t {
+    return row ? tr * NN + n : (tr / C) * NN * C + n * C + tr % C;
+  };
+  p.gstride = (N / rad[0]) * (row ? 1 : C);
+  p.ostride = (N / rad[S - 1]) * (row ? 1 : C);
+  // Load mechanism: a contiguous chunk uses a flat 2D tensor map [total/W][W];
+  // a column strip (C < cols) uses a 3D box {C, rows, 1}.
+  int64_t total = row ? count * (int64_t)N : images * (int64_t)N * cols;
+  p.flat = row || p.C == cols;
+  if (p.flat) {
+    // W = 32: [total/32][32] view, 128B swizzle; W = 4: [total/4][4];
+    // W = 1: rank-1 view [total] in 256-element boxes (any total).
+    // (row passes with N < 32 stay unswizzled: the kernel's compile-time row
+    // addressing assumes the 128B swizzle exactly when N >= 32)
+    const bool can32 = (total % 32 == 0) && (!row || N >= 32);
+    p.W = can32 ? 32 : (total % 4 == 0 ? 4 : 1);
+    p.swz_in = p.swz_out = p.W == 32 ? 0x70 : 0;
+    p.box_rows = std::min(E / p.W, 256);
+    p.n_sub = (E / p.W) / p.box_rows;
+    p.sub_bytes = p.box_rows * p.W * 4;
+  } else {
+    int run = C * 4;
+    p.swz_in = p.swz_out = run == 128 ? 0x70 : run == 64 ? 0x30 : run == 32 ? 0x10 : 0;
+    p.box_rows = std::min(N, 256);
+    p.n_sub = N / p.box_rows;
+    p.sub_bytes = p.box_rows * C * 4;
+  }
+  p.total = total;
+
+  int n2 = 1, tiles_max = 0;
+  for (int s = 0; s < S; ++s) {
+    StageInfo& st = p.st[s];
+    st.R = rad[s];
+    st.n2 = n2;
+    n2 *= rad[s];
+    st.KP = std::max(2 * st.R, 16);
+    st.NP = std::max(2 * st.R, 16);
+    if (E % (kLanes * st.R)) {
+      if (err) *err = "chunk not a whole number of tiles";
+      return false;
+    }
+    st.tiles = E / (kLanes * st.R);
+    tiles_max = std::max(tiles_max, st.tiles);
+    if (s > 0 && st.R < 8) {
+      if (err) *err = "radix < 8 only supported as a single stage";
+      return false;
+    }
+    st.sbo = 32 * st.R + 16;
+    st.tile_bytes = 16 * st.sbo;
+    st.t_off = -1;
+    st.hstep = st.im_off = 0;
+  }
+  p.tiles_max = tiles_max;
+
+  // ---- row identities per stage, writer tables -------------------------
+  p.rows_tab.assign((size_t)S * tiles_max * kLanes, RowInfo{});
+  auto rec = [&](int s, int row) -> RowInfo& {
+    return p.rows_tab[((size_t)s * tiles_max + row / kLanes) * kLanes + row % kLanes];
+  };
+  // stage-1 butterflies: blk in [0, N/R1); natural base b(blk)
+  const int R1 = rad[0];
+  std::vector<int> P(S);
+  for (int i = 0; i < S; ++i) {
+    int prod = 1;
+    for (int l = i + 1; l < S; ++l) prod *= rad[l];
+    P[i] = prod;
+  }
+  auto bnat = [&](int blk) {
+    int b = 0, rem = blk;
+    for (int i = 1; i < S; ++i) {
+      int d = rem % rad[i];
+      rem /= rad[i];
+      b += d * P[i];
+    }
+    return b;
+  };
+  std::vector<Bf> cur;
+  cur.reserve(E / R1);
+  {
+    std::vector<std::tuple<int32_t, int, int>> order;
+    for (int tr = 0; tr < T; ++tr)
+      for (int blk = 0; blk < N / R1; ++blk) order.emplace_back(w_addr(tr, bnat(blk)), tr, blk);
+    std::sort(order.begin(), order.end());
+    for (auto& o : order) cur.push_back(Bf{std::get<1>(o), 0, std::get<2>(o)});
+  }
+  for (size_t i = 0; i < cur.size(); ++i) rec(0, (int)i).gbase = w_addr(cur[i].tr, bnat(cur[i].blk));
+
+  for (int s = 0; s + 1 < S; ++s) {
+    StageInfo& st = p.st[s];
+    StageInfo& nx_ = p.st[s + 1];
+    const int R = st.R, Rn = nx_.R, G = kLanes / R;
+    const int n2n = st.n2 * R;  // n2 of the next stage
+    std::map<std::tuple<int, int, int>, int> gid;
+    std::vector<Bf> nxt(E / Rn);
+    st.hstep = G * nx_.sbo;
+    st.im_off = Rn * 16;
+    for (size_t rho = 0; rho < cur.size(); ++rho) {
+      const Bf& w = cur[rho];
+      int mp = w.blk % Rn, blkn = w.blk / Rn;
+      auto key = std::make_tuple(w.tr, w.k, blkn);
+      auto it = gid.find(key);
+      int g;
+      if (it == gid.end()) {
+        g = (int)gid.size();
+        gid.emplace(key, g);
+        for (int j = 0; j < R; ++j) {
+          int idx = (g / G) * kLanes + ((g % G) + G * (j / 8)) * 8 + j % 8;
+          nxt[idx] = Bf{w.tr, w.k + st.n2 * j, blkn};
+        }
+      } else {
+        g = it->second;
+      }
+      RowInfo& r = rec(s, (int)rho);
+      r.addr = (g / G) * nx_.tile_bytes + (g % G) * nx_.sbo + mp * 16;
+      r.mp = mp;
+      r.tw = s > 0 ? 1 : 0;
+      double cr, ci, wr, wi;
+      root((int64_t)mp * w.k, (int64_t)Rn * n2n, &cr, &ci);
+      root((int64_t)mp, (int64_t)Rn * R, &wr, &wi);
+      r.cr = (float)cr;
+      r.ci = (float)ci;
+      r.wr = (float)wr;
+      r.wi = (float)wi;
+    }
+    cur.swap(nxt);
+  }
+  for (size_t i = 0; i < cur.size(); ++i) rec(S - 1, (int)i).addr = w_addr(cur[i].tr, cur[i].k);
+
+  // ---- B matrices ---------------------------------------------------------
+  p.bblob.clear();
+  for (int s = 0; s < S; ++s) {
+    StageInfo& st = p.st[s];
+    const int R = st.R, KP = st.KP, NP = st.NP;
+    st.b_off = (int)(p.bblob.size() * 2);
+    st.b_bytes = KP * NP * 2;
+    std::vector<uint16_t> blob(KP * NP, 0);
+    for (int k = 0; k < KP; ++k)
+      for (int n = 0; n < NP; ++n) {
+        double v = 0.0;
+        if (k < 2 * R && n < 2 * R) {
+          int m, cin;
+          if (s == 0) {
+            m = k / 2;
+            cin = k % 2;
+          } else {
+            m = k % R;
+            cin = k / R;
+          }
+          int j = n % R, cout = n / R;
+          double fr, fi;
+          root((int64_t)j * m, R, &fr, &fi);
+          double Fr = f16_to_f64(f64_to_f16_rne(fr)), Fi = f16_to_f64(f64_to_f16_rne(fi));
+          if (cin == 0 && cout == 0) v = Fr;
+          if (cin == 1 && cout == 0) v = -Fi;
+          if (cin == 0 && cout == 1) v = Fi;
+          if (cin == 1 && cout == 1) v = Fr;
+        }
+        int q = k / 16, kk = k % 16;
+        size_t off = (size_t)q * 32 * NP + (n % 8) * 16 + (n / 8) * 256 + (kk / 8) * 128 + (kk % 8) * 2;
+        blob[off / 2] = f64_to_f16_rne(v);
+      }
+    p.bblob.insert(p.bblob.end(), blob.begin(), blob.end());
+  }
+
+  p.tblob.clear();  // twiddles come from the per-row (c, w) recurrence
+
+  // ---- shared memory / TMEM budget ---------------------------------------
+  int a_bytes = E * 4;
+  for (int s = 1; s < S; ++s) a_bytes = std::max(a_bytes, p.st[s].tiles * p.st[s].tile_bytes);
+  a_bytes = (a_bytes + 1023) & ~1023;
+  p.a_bytes = a_bytes;
+  p.smem_in = 0;
+  p.smem_a = E * 4;
+  p.smem_b = p.smem_a + a_bytes;
+  int bsz = ((int)p.bblob.size() * 2 + 127) & ~127;
+  p.smem_t = p.smem_b + bsz;
+  p.smem_bar = p.smem_t;
+  p.smem_bytes = p.smem_bar + 64 /*mbarriers + TMEM address*/ + 1024 /*alignment slack*/;
+  int acols = p.st[0].tiles * (p.st[0].KP / 2);
+  int dcols = 0;
+  for (int s = 0; s < S; ++s) dcols = std::max(dcols, p.st[s].tiles * p.st[s].NP);
+  int need = acols + dcols, tcols = 32;
+  while (tcols < need) tcols <<= 1;
+  if (tcols > 512) {
+    if (err) *err = "TMEM budget exceeded";
+    return false;
+  }
+  p.tmem_cols = tcols;
+  p.tmem_a_cols = dcols;  // A region starts after D
+  int by_tmem = 512 / tcols;
+  int by_smem = (227 * 1024) / p.smem_bytes;
+  p.ctas_per_sm = std::max(1, std::min(by_tmem, std::min(by_smem, 4)));
+  return true;
+}
+
+int build_plan(Plan& plan, int dims, int nx, int ny, int64_t batch, std::string* err) {
+  plan = Plan();
+  plan.dims = dims;
+  plan.nx = nx;
+  plan.ny = ny;
+  plan.batch = batch;
+  auto pow2 = [](int n) { return n >= 2 && (n & (n - 1)) == 0; };
+  if (!pow2(nx) || (dims == 2 && !pow2(ny))) {
+    if (err) *err = "sizes must be powers of two >= 2";
+    return 4;  // TCFFT_INVALID_SIZE
+  }
+  if (batch < 1) {
+    if (err) *err = "batch must be >= 1";
+    return 3;  // TCFFT_INVALID_VALUE
+  }
+  if (dims == 1) {
+    PassPlan p;
+    if (!build_pass(p, kPassRow, nx, batch, 0, 0, err)) return 6;  // NOT_SUPPORTED
+    plan.passes.push_back(std::move(p));
+    return 0;
+  }
+  // 2D, row-major (nx, ny): contiguous rows (ny) first, then columns (nx)
+  // at stride ny (reference executor.py:180-190).
+  PassPlan rowp, colp;
+  if (!build_pass(rowp, kPassRow, ny, batch * (int64_t)nx, 0, 0, err)) return 6;
+  if (!build_pass(colp, kPassStrip, nx, 0, batch, ny, err)) return 6;
+  plan.passes.push_back(std::move(rowp));
+  plan.passes.push_back(std::move(colp));
+  return 0;
+}
+
+}  // namespace tcfft

@@ -1,0 +1,98 @@
+// plan.hpp - host-side planner for the B200 tcFFT passes (no CUDA dependency).
+//
+// A plan is a list of passes; a pass is one persistent kernel launch that
+// reads every element once from HBM and writes it once.  Inside a pass each
+// CTA loops over "chunks" of E complex elements (several short transforms or a
+// strip of columns), runs S DFT-as-GEMM stages on the tensor cores and stores
+// the chunk back.  All index math (which butterfly a TMEM lane owns at each
+// stage, where its outputs go, which twiddle they need) is resolved here, on
+// the host, into small per-(stage, tile, lane) tables, so the kernel only does
+// affine address arithmetic.  See DESIGN.md for the dataflow.
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+
+namespace tcfft {
+
+constexpr int kMaxStages = 3;
+constexpr int kLanes = 128;  // M of every tcgen05.mma tile
+
+enum PassKind : int32_t {
+  kPassRow = 0,    // contiguous transforms: element n of transform tr at tr*N + n
+  kPassStrip = 1,  // column strip: element n of column tr at n*C + tr (2D column pass)
+};
+
+struct StageInfo {
+  int32_t R;        // radix
+  int32_t n2;       // product of earlier radices (reference kernels.py:323 "n2")
+  int32_t KP, NP;   // MMA K and N (2R padded up to 16)
+  int32_t tiles;    // E / (128 R)
+  int32_t sbo;      // A operand stride between 8-row core-matrix groups (bytes), SS stages
+  int32_t tile_bytes;  // A operand bytes per 128-row tile
+  int32_t b_off;    // byte offset of this stage's B matrix in the B blob
+  int32_t b_bytes;
+  int32_t t_off;    // byte offset of the writer twiddle table (float4 [R'][R/2]); -1 if final
+  int32_t hstep;    // writer: byte step between successive 8-output chunks
+  int32_t im_off;   // writer: byte offset of the imaginary plane (R' * 16)
+};
+
+// Per (stage, tile, lane) row record, 32 bytes, read once per CTA.
+struct RowInfo {
+  int32_t gbase;  // stage 1: word address (staging) of input m = 0
+  int32_t addr;   // writer: byte offset of its first 16B chunk in the next A tile;
+                  // final stage: word address (staging) of output j = 0
+  int32_t mp;     // writer: next-stage input index m'
+  int32_t tw;     // 1 if the writer's c differs from 1 (stage >= 2)
+  float cr, ci;   // writer: twiddle of output j = 0, c = W_{R' n2'}^{m' k}
+  float wr, wi;   // writer: per-output ratio w = W_{R R'}^{m'}; output j gets c * w^j
+};
+
+struct PassPlan {
+  int32_t kind;     // PassKind
+  int32_t N;        // transform length of this pass
+  int32_t E;        // complex elements per chunk
+  int32_t T;        // transforms per chunk
+  int32_t S;        // stages
+  StageInfo st[kMaxStages];
+  int32_t gstride;  // staging words between successive gather inputs m
+  int32_t ostride;  // staging words between successive final outputs j
+  int32_t swz_in, swz_out;  // 128B/64B/32B swizzle masks (0x70/0x30/0x10) or 0
+  int64_t count;    // transforms in the pass (row) or columns (strip)
+  int64_t chunks;
+  // strip geometry (kind == kPassStrip): images x rows(=N) x cols, C columns
+  // of IMG images per chunk
+  int64_t images;
+  int32_t rows, cols, C, IMG;
+  // TMA: flat contiguous chunk ([total/W][W] view) or 3D column box
+  int32_t flat, W, box_rows, n_sub, sub_bytes;
+  int64_t total;
+  // shared-memory carve-up (bytes, relative to the 1024-aligned base)
+  int32_t smem_in, smem_a, smem_b, smem_t, smem_bar, smem_bytes;
+  int32_t a_bytes;   // A buffer size (>= E*4, also used as output staging)
+  int32_t tmem_cols; // allocation (power of two >= 32)
+  int32_t tmem_a_cols;
+  int32_t ctas_per_sm;
+  std::vector<RowInfo> rows_tab;   // [S][tiles_max][128]
+  int32_t tiles_max;
+  std::vector<uint16_t> bblob;     // fp16 B matrices, UMMA K-major core-matrix order
+  std::vector<float> tblob;        // writer twiddle tables, 8 floats per (m', j-pair)
+};
+
+struct Plan {
+  int32_t dims = 1;
+  int32_t nx = 0, ny = 0;
+  int64_t batch = 0;
+  std::vector<PassPlan> passes;
+};
+
+// Radix list chosen for a single-pass transform of length n (product == n).
+std::vector<int> choose_radices(int n);
+int chunk_elems_for(int n);
+
+// Builds a pass.  kind/geometry as in PassPlan; returns false on unsupported size.
+bool build_pass(PassPlan& p, int kind, int N, int64_t count, int64_t images, int cols, std::string* err);
+// Builds the whole plan (host-only, no CUDA calls).
+int build_plan(Plan& plan, int dims, int nx, int ny, int64_t batch, std::string* err);
+
+}  // namespace tcfft

@@ -1,0 +1,353 @@
+// tcfft_api.cu - C ABI (include/tcfft_b200.h): plan objects, device tables,
+// TMA tensor maps and kernel dispatch for the sm_100a FFT passes.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/tcfft_b200.h"
+#include "fft_kernel.cuh"
+#include "plan.hpp"
+
+using tcfft::KParams;
+using tcfft::PassPlan;
+
+namespace {
+
+using KernelFn = void (*)(CUtensorMap, CUtensorMap, KParams);
+
+struct KernelEntry {
+  int E, R1, R2, R3, row;
+  const void* fn;
+  void (*launch)(dim3, int, cudaStream_t, const CUtensorMap&, const CUtensorMap&, const KParams&);
+};
+
+template <int E, int R1, int R2, int R3, int MINB, bool ROW>
+void launch_tpl(dim3 grid, int smem, cudaStream_t st, const CUtensorMap& a, const CUtensorMap& b,
+                const KParams& p) {
+  tcfft::fft_pass_kernel<E, R1, R2, R3, MINB, ROW><<<grid, 128, smem, st>>>(a, b, p);
+}
+
+#define KENTRY(E, R1, R2, R3, MB, ROW)                                                                     \
+  {                                                                                                        \
+    E, R1, R2, R3, ROW, (const void*)&tcfft::fft_pass_kernel<E, R1, R2, R3, MB, ROW>,                     \
+        &launch_tpl<E, R1, R2, R3, MB, ROW>                                                                \
+  }
+#define KBOTH(E, R1, R2, R3, MB) KENTRY(E, R1, R2, R3, MB, true), KENTRY(E, R1, R2, R3, MB, false)
+
+// Every (chunk size, radix list) the planner can emit, for contiguous row
+// passes (compile-time strides) and column-strip passes.
+const KernelEntry kKernels[] = {
+    KBOTH(1024, 2, 0, 0, 4),     KBOTH(2048, 4, 0, 0, 4),     KBOTH(4096, 8, 0, 0, 4),
+    KBOTH(4096, 16, 0, 0, 4),    KBOTH(4096, 32, 0, 0, 4),    KBOTH(4096, 8, 8, 0, 4),
+    KBOTH(4096, 16, 8, 0, 4),    KBOTH(4096, 16, 16, 0, 4),   KBOTH(4096, 16, 32, 0, 4),
+    KBOTH(4096, 32, 32, 0, 4),   KBOTH(4096, 16, 16, 8, 4),   KBOTH(4096, 16, 16, 16, 4),
+    KENTRY(8192, 16, 16, 32, 2, true),   KENTRY(8192, 16, 16, 8, 2, false),
+    KENTRY(16384, 16, 32, 32, 1, true),  KENTRY(16384, 16, 16, 16, 1, false),
+};
+
+const KernelEntry* find_kernel(const PassPlan& p) {
+  int r[3] = {0, 0, 0};
+  for (int s = 0; s < p.S; ++s) r[s] = p.st[s].R;
+  const int row = p.kind == tcfft::kPassRow ? 1 : 0;
+  for (const auto& k : kKernels)
+    if (k.E == p.E && k.R1 == r[0] && k.R2 == r[1] && k.R3 == r[2] && k.row == row) return &k;
+  return nullptr;
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+  });
+  return fn;
+}
+
+struct DevPass {
+  const KernelEntry* k = nullptr;
+  void* tables = nullptr;  // rows | bblob | tblob
+  KParams kp{};
+  int grid = 0;
+};
+
+}  // namespace
+
+struct tcfftPlanImpl {
+  tcfft::Plan plan;
+  std::vector<DevPass> dev;
+  cudaStream_t stream = nullptr;
+  int device = 0;
+  int magic = 0x7cff7;
+};
+
+namespace {
+
+tcfftResult make_tmap(CUtensorMap* tm, const PassPlan& p, const void* base) {
+  auto enc = encode_fn();
+  if (!enc) return TCFFT_EXEC_FAILED;
+  CUresult r;
+  if (p.flat && p.W == 1) {
+    cuuint64_t dims[1] = {(cuuint64_t)p.total};
+    cuuint64_t strides[1] = {0};
+    cuuint32_t box[1] = {(cuuint32_t)p.box_rows};
+    cuuint32_t es[1] = {1};
+    r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_UINT32, 1, const_cast<void*>(base), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  } else if (p.flat) {
+    cuuint64_t dims[2] = {(cuuint64_t)p.W, (cuuint64_t)(p.total / p.W)};
+    cuuint64_t strides[1] = {(cuuint64_t)p.W * 4};
+    cuuint32_t box[2] = {(cuuint32_t)p.W, (cuuint32_t)p.box_rows};
+    cuuint32_t es[2] = {1, 1};
+    r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<void*>(base), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, p.W == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  } else {
+    cuuint64_t dims[3] = {(cuuint64_t)p.cols, (cuuint64_t)p.rows, (cuuint64_t)p.images};
+    cuuint64_t strides[2] = {(cuuint64_t)p.cols * 4, (cuuint64_t)p.cols * p.rows * 4};
+    cuuint32_t box[3] = {(cuuint32_t)p.C, (cuuint32_t)p.box_rows, 1};
+    cuuint32_t es[3] = {1, 1, 1};
+    int run = p.C * 4;
+    CUtensorMapSwizzle sw = run == 128  ? CU_TENSOR_MAP_SWIZZLE_128B
+                            : run == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                            : run == 32 ? CU_TENSOR_MAP_SWIZZLE_32B
+                                        : CU_TENSOR_MAP_SWIZZLE_NONE;
+    r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, const_cast<void*>(base), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  }
+  return r == CUDA_SUCCESS ? TCFFT_SUCCESS : TCFFT_EXEC_FAILED;
+}
+
+tcfftResult map_build_status(int st) {
+  switch (st) {
+    case 0: return TCFFT_SUCCESS;
+    case 3: return TCFFT_INVALID_VALUE;
+    case 4: return TCFFT_INVALID_SIZE;
+    default: return TCFFT_NOT_SUPPORTED;
+  }
+}
+
+tcfftResult create(tcfftHandle* out, int dims, int nx, int ny, int batch) {
+  if (!out) return TCFFT_INVALID_VALUE;
+  *out = nullptr;
+  auto* h = new (std::nothrow) tcfftPlanImpl();
+  if (!h) return TCFFT_ALLOC_FAILED;
+  std::string err;
+  tcfftResult st = map_build_status(tcfft::build_plan(h->plan, dims, nx, ny, batch, &err));
+  if (st != TCFFT_SUCCESS) {
+    delete h;
+    return st;
+  }
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    delete h;
+    return TCFFT_NO_DEVICE;
+  }
+  cudaGetDevice(&h->device);
+  cudaDeviceProp prop;
+  cudaGetDeviceProperties(&prop, h->device);
+  if (prop.major != 10) {
+    delete h;
+    return TCFFT_NO_DEVICE;
+  }
+  for (const PassPlan& p : h->plan.passes) {
+    DevPass d;
+    d.k = find_kernel(p);
+    if (!d.k) {
+      delete h;
+      return TCFFT_NOT_SUPPORTED;
+    }
+    size_t rb = p.rows_tab.size() * sizeof(tcfft::RowInfo);
+    size_t bb = (p.bblob.size() * 2 + 255) & ~size_t(255);
+    size_t tb = (p.tblob.size() * 4 + 255) & ~size_t(255);
+    size_t rb_al = (rb + 255) & ~size_t(255);
+    if (cudaMalloc(&d.tables, rb_al + bb + tb + 256) != cudaSuccess) {
+      cudaGetLastError();
+      for (auto& q : h->dev) cudaFree(q.tables);
+      delete h;
+      return TCFFT_ALLOC_FAILED;
+    }
+    char* base = static_cast<char*>(d.tables);
+    cudaMemcpy(base, p.rows_tab.data(), rb, cudaMemcpyHostToDevice);
+    cudaMemcpy(base + rb_al, p.bblob.data(), p.bblob.size() * 2, cudaMemcpyHostToDevice);
+    if (!p.tblob.empty()) cudaMemcpy(base + rb_al + bb, p.tblob.data(), p.tblob.size() * 4, cudaMemcpyHostToDevice);
+    KParams& k = d.kp;
+    std::memset(&k, 0, sizeof(k));
+    k.chunks = p.chunks;
+    k.flat = p.flat ? (p.W == 1 ? 2 : 1) : 0;
+    k.chunk_rows = p.flat ? p.E / p.W : 0;
+    k.strips_per_image = p.flat ? 1 : p.cols / p.C;
+    k.C = p.C;
+    k.gstride = p.gstride;
+    k.ostride = p.ostride;
+    k.swz = p.swz_in;
+    k.tiles_max = p.tiles_max;
+    k.box_rows = p.box_rows;
+    k.n_sub = p.n_sub;
+    k.sub_bytes = p.sub_bytes;
+    k.rows_tab = reinterpret_cast<const tcfft::RowInfo*>(base);
+    k.bblob = reinterpret_cast<const uint16_t*>(base + rb_al);
+    k.bbytes = (int)(p.bblob.size() * 2);  // multiple of 512
+    k.smem_a = p.smem_a;
+    k.smem_b = p.smem_b;
+    k.smem_bar = p.smem_bar;
+    cudaFuncSetAttribute(d.k->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, p.smem_bytes);
+    int64_t slots = (int64_t)prop.multiProcessorCount * p.ctas_per_sm;
+    d.grid = (int)std::min<int64_t>(p.chunks, slots);
+    h->dev.push_back(d);
+  }
+  if (cudaGetLastError() != cudaSuccess) {
+    for (auto& q : h->dev) cudaFree(q.tables);
+    delete h;
+    return TCFFT_EXEC_FAILED;
+  }
+  *out = h;
+  return TCFFT_SUCCESS;
+}
+
+bool valid(tcfftHandle h) { return h && h->magic == 0x7cff7; }
+
+}  // namespace
+
+extern "C" {
+
+tcfftResult tcfftPlan1D(tcfftHandle* plan, int nx, int batch) { return create(plan, 1, nx, 0, batch); }
+tcfftResult tcfftPlan2D(tcfftHandle* plan, int nx, int ny, int batch) { return create(plan, 2, nx, ny, batch); }
+
+tcfftResult tcfftSetStream(tcfftHandle plan, void* stream) {
+  if (!valid(plan)) return TCFFT_INVALID_PLAN;
+  plan->stream = static_cast<cudaStream_t>(stream);
+  return TCFFT_SUCCESS;
+}
+
+tcfftResult tcfftGetWorkspaceSize(tcfftHandle plan, size_t* bytes) {
+  if (!valid(plan)) return TCFFT_INVALID_PLAN;
+  if (!bytes) return TCFFT_INVALID_VALUE;
+  *bytes = 0;
+  return TCFFT_SUCCESS;
+}
+
+tcfftResult tcfftExecC2C(tcfftHandle plan, const void* idata, void* odata) {
+  if (!valid(plan)) return TCFFT_INVALID_PLAN;
+  if (!idata || !odata) return TCFFT_INVALID_VALUE;
+  if ((reinterpret_cast<uintptr_t>(idata) | reinterpret_cast<uintptr_t>(odata)) & 15) return TCFFT_INVALID_VALUE;
+  for (size_t i = 0; i < plan->dev.size(); ++i) {
+    const PassPlan& p = plan->plan.passes[i];
+    const DevPass& d = plan->dev[i];
+    const void* src = (i == 0) ? idata : odata;
+    CUtensorMap tin, tout;
+    if (make_tmap(&tin, p, src) != TCFFT_SUCCESS || make_tmap(&tout, p, odata) != TCFFT_SUCCESS)
+      return TCFFT_EXEC_FAILED;
+    d.k->launch(dim3(d.grid), p.smem_bytes, plan->stream, tin, tout, d.kp);
+    if (cudaGetLastError() != cudaSuccess) return TCFFT_EXEC_FAILED;
+  }
+  return TCFFT_SUCCESS;
+}
+
+tcfftResult tcfftDestroy(tcfftHandle plan) {
+  if (!valid(plan)) return TCFFT_INVALID_PLAN;
+  for (auto& q : plan->dev) cudaFree(q.tables);
+  plan->magic = 0;
+  delete plan;
+  return TCFFT_SUCCESS;
+}
+
+const char* tcfftGetErrorString(tcfftResult r) {
+  switch (r) {
+    case TCFFT_SUCCESS: return "TCFFT_SUCCESS";
+    case TCFFT_INVALID_PLAN: return "TCFFT_INVALID_PLAN";
+    case TCFFT_ALLOC_FAILED: return "TCFFT_ALLOC_FAILED";
+    case TCFFT_INVALID_VALUE: return "TCFFT_INVALID_VALUE";
+    case TCFFT_INVALID_SIZE: return "TCFFT_INVALID_SIZE";
+    case TCFFT_EXEC_FAILED: return "TCFFT_EXEC_FAILED";
+    case TCFFT_NOT_SUPPORTED: return "TCFFT_NOT_SUPPORTED";
+    case TCFFT_NO_DEVICE: return "TCFFT_NO_DEVICE";
+  }
+  return "unknown tcfftResult";
+}
+
+int tcfftGetVersion(void) { return 100; }
+
+tcfftResult tcfftDescribePlan(int dims, int nx, int ny, int batch, char* json, size_t cap) {
+  tcfft::Plan plan;
+  std::string err;
+  tcfftResult st = map_build_status(tcfft::build_plan(plan, dims, nx, ny, batch, &err));
+  std::string s;
+  if (st != TCFFT_SUCCESS) {
+    s = "{\"error\": \"" + err + "\"}";
+  } else {
+    s = "{\"dims\": " + std::to_string(dims) + ", \"nx\": " + std::to_string(nx) + ", \"ny\": " +
+        std::to_string(ny) + ", \"batch\": " + std::to_string(batch) + ", \"passes\": [";
+    for (size_t i = 0; i < plan.passes.size(); ++i) {
+      const PassPlan& p = plan.passes[i];
+      if (i) s += ", ";
+      s += "{\"kind\": \"" + std::string(p.kind == tcfft::kPassRow ? "row" : "strip") + "\", \"N\": " +
+           std::to_string(p.N) + ", \"E\": " + std::to_string(p.E) + ", \"T\": " + std::to_string(p.T) +
+           ", \"C\": " + std::to_string(p.C) + ", \"IMG\": " + std::to_string(p.IMG) +
+           ", \"chunks\": " + std::to_string(p.chunks) + ", \"flat\": " + std::to_string(p.flat) +
+           ", \"W\": " + std::to_string(p.W) + ", \"gstride\": " + std::to_string(p.gstride) +
+           ", \"ostride\": " + std::to_string(p.ostride) + ", \"swz\": " + std::to_string(p.swz_in) +
+           ", \"smem_bytes\": " + std::to_string(p.smem_bytes) + ", \"smem_a\": " + std::to_string(p.smem_a) +
+           ", \"a_bytes\": " + std::to_string(p.a_bytes) + ", \"tmem_cols\": " + std::to_string(p.tmem_cols) +
+           ", \"tmem_a_col\": " + std::to_string(p.tmem_a_cols) +
+           ", \"ctas_per_sm\": " + std::to_string(p.ctas_per_sm) + ", \"tiles_max\": " +
+           std::to_string(p.tiles_max) + ", \"stages\": [";
+      for (int sidx = 0; sidx < p.S; ++sidx) {
+        const auto& t = p.st[sidx];
+        if (sidx) s += ", ";
+        s += "{\"R\": " + std::to_string(t.R) + ", \"n2\": " + std::to_string(t.n2) + ", \"KP\": " +
+             std::to_string(t.KP) + ", \"NP\": " + std::to_string(t.NP) + ", \"tiles\": " +
+             std::to_string(t.tiles) + ", \"sbo\": " + std::to_string(t.sbo) + ", \"tile_bytes\": " +
+             std::to_string(t.tile_bytes) + ", \"b_off\": " + std::to_string(t.b_off) + ", \"t_off\": " +
+             std::to_string(t.t_off) + ", \"hstep\": " + std::to_string(t.hstep) + ", \"im_off\": " +
+             std::to_string(t.im_off) + "}";
+      }
+      s += "]}";
+    }
+    s += "]}";
+  }
+  if (json && cap) {
+    std::strncpy(json, s.c_str(), cap - 1);
+    json[cap - 1] = 0;
+  }
+  if (!json && cap == 0) return st;
+  return s.size() < cap ? st : TCFFT_INVALID_VALUE;
+}
+
+tcfftResult tcfftPlanTables(int dims, int nx, int ny, int batch, int pass, void* rows, size_t* rows_bytes,
+                            void* bmats, size_t* b_bytes, void* twid, size_t* t_bytes) {
+  tcfft::Plan plan;
+  std::string err;
+  tcfftResult st = map_build_status(tcfft::build_plan(plan, dims, nx, ny, batch, &err));
+  if (st != TCFFT_SUCCESS) return st;
+  if (pass < 0 || pass >= (int)plan.passes.size()) return TCFFT_INVALID_VALUE;
+  const PassPlan& p = plan.passes[pass];
+  size_t rb = p.rows_tab.size() * sizeof(tcfft::RowInfo), bb = p.bblob.size() * 2, tb = p.tblob.size() * 4;
+  if (rows_bytes) {
+    if (rows && *rows_bytes >= rb) std::memcpy(rows, p.rows_tab.data(), rb);
+    *rows_bytes = rb;
+  }
+  if (b_bytes) {
+    if (bmats && *b_bytes >= bb) std::memcpy(bmats, p.bblob.data(), bb);
+    *b_bytes = bb;
+  }
+  if (t_bytes) {
+    if (twid && *t_bytes >= tb) std::memcpy(twid, p.tblob.data(), tb);
+    *t_bytes = tb;
+  }
+  return TCFFT_SUCCESS;
+}
+
+}  // extern "C"

@@ -1,0 +1,189 @@
+"""CPU emulation of the sm_100a pass kernel's dataflow, driven by the very
+host tables the C planner builds (tcfftPlanTables / tcfftDescribePlan).
+
+Test infrastructure: it lets the CPU suite check every index map (stage-1
+gather addresses, writer destinations in the MN-major A operand, twiddle
+tables, DFT block matrices, 128B-swizzled staging, output addresses) end to
+end without a GPU, and measures shared-memory bank conflicts of each access
+pattern.  The tcgen05 operand layouts it assumes (K-major B, MN-major A with
+padded SBO, A-from-TMEM packing) are the ones tests/native/umma_probe.cu
+verifies on the hardware.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from paper_2104_11471_b200 import _lib
+
+ROW_DT = np.dtype([("gbase", "<i4"), ("addr", "<i4"), ("mp", "<i4"), ("tw", "<i4"), ("cr", "<f4"),
+                   ("ci", "<f4"), ("wr", "<f4"), ("wi", "<f4")])
+
+
+class PassTables:
+    def __init__(self, dims, nx, ny, batch, index):
+        desc = _lib.describe(dims, nx, ny, batch)
+        self.d = desc["passes"][index]
+        rows, b, t = _lib.plan_tables(dims, nx, ny, batch, index)
+        S, tm = len(self.d["stages"]), self.d["tiles_max"]
+        self.rows = np.frombuffer(rows, dtype=ROW_DT).reshape(S, tm, 128)
+        self.b = np.frombuffer(b, dtype=np.float16)
+        self.t = np.frombuffer(t, dtype=np.float32) if len(t) else np.zeros(0, np.float32)
+
+    def bmat(self, s):
+        st = self.d["stages"][s]
+        KP, NP = st["KP"], st["NP"]
+        k = np.arange(KP)[:, None]
+        n = np.arange(NP)[None, :]
+        off = (k // 16) * 32 * NP + (n % 8) * 16 + (n // 8) * 256 + ((k % 16) // 8) * 128 + (k % 8) * 2
+        return self.b[(st["b_off"] + off) // 2].astype(np.float64)  # (KP, NP)
+
+
+def _swz(b, mask):
+    return b ^ ((b >> 3) & mask)
+
+
+def _half(x):
+    with np.errstate(over="ignore"):
+        return np.asarray(x, dtype=np.float32).astype(np.float16)
+
+
+def emulate_chunk(pt: PassTables, chunk_words: np.ndarray, stats: dict | None = None) -> np.ndarray:
+    """chunk_words: (E,) uint32 interleaved fp16 pairs in linear staging order.
+    Returns the (E,) uint32 output staging in linear order."""
+    d = pt.d
+    E, swz = d["E"], d["swz"]
+    stages = d["stages"]
+    S = len(stages)
+    lin = np.arange(E, dtype=np.int64) * 4
+    sbuf = np.zeros(E, np.uint32)
+    sbuf[_swz(lin, swz) // 4] = chunk_words
+
+    # ---- stage 1 gather -> A (TMEM), interleaved K
+    st = stages[0]
+    R, T1, KP = st["R"], st["tiles"], st["KP"]
+    rec = pt.rows[0, :T1]
+    addr = (rec["gbase"][..., None].astype(np.int64) + np.arange(R) * d["gstride"]) * 4
+    phys = _swz(addr, swz)
+    if stats is not None:
+        _bank_stats(stats, "gather_lds32", phys, 4)
+    w = sbuf[phys // 4]  # (T1, 128, R)
+    pairs = w.view(np.float16).reshape(T1, 128, R, 2).astype(np.float64)
+    A = np.zeros((T1, 128, KP))
+    A[..., : 2 * R] = pairs.reshape(T1, 128, 2 * R)
+    D = A @ pt.bmat(0)
+
+    abuf = None
+    for s in range(S - 1):
+        st, nx_ = stages[s], stages[s + 1]
+        R, Rn, T = st["R"], nx_["R"], st["tiles"]
+        rec = pt.rows[s, :T]
+        xr = D[..., :R].astype(np.float32)
+        xi = D[..., R: 2 * R].astype(np.float32)
+        # kernel: output j gets c * w^j (register recurrence; c = 1 at stage 1)
+        c = (rec["cr"] + 1j * rec["ci"]) if s > 0 else np.ones(rec.shape)
+        w = rec["wr"] + 1j * rec["wi"]
+        tw = (c[..., None] * w[..., None] ** np.arange(R)).astype(np.complex64)
+        trr, tii = tw.real, tw.imag
+        yr = xr * trr - xi * tii
+        yi = xr * tii + xi * trr
+        hr, hi = _half(yr), _half(yi)
+        abytes = nx_["tiles"] * nx_["tile_bytes"]
+        abuf = np.zeros(abytes // 2, np.float16)
+        a0 = rec["addr"].astype(np.int64)
+        st_addr = []
+        for h in range(R // 8):
+            base = a0 + h * st["hstep"]
+            st_addr.append(base)
+            st_addr.append(base + st["im_off"])
+            for j8 in range(8):
+                j = 8 * h + j8
+                abuf[(base + j8 * 2) // 2] = hr[..., j]
+                abuf[(base + st["im_off"] + j8 * 2) // 2] = hi[..., j]
+        if stats is not None:
+            _bank_stats(stats, "writer_sts128", np.stack(st_addr, -1), 16)
+        # next stage: A (MN-major, split planes), D = A @ B
+        Tn, KPn, sbo, tb = nx_["tiles"], nx_["KP"], nx_["sbo"], nx_["tile_bytes"]
+        t = np.arange(Tn)[:, None, None]
+        row = np.arange(128)[None, :, None]
+        k = np.arange(KPn)[None, None, :]
+        off = t * tb + (row // 8) * sbo + (row % 8) * 2 + k * 16
+        A = abuf[off // 2].astype(np.float64)
+        D = A @ pt.bmat(s + 1)
+
+    st = stages[S - 1]
+    R, T = st["R"], st["tiles"]
+    rec = pt.rows[S - 1, :T]
+    hr, hi = _half(D[..., :R]), _half(D[..., R: 2 * R])
+    words = np.stack([hr, hi], -1).view(np.uint32)[..., 0]  # (T,128,R)
+    oaddr = (rec["addr"][..., None].astype(np.int64) + np.arange(R) * d["ostride"]) * 4
+    ophys = _swz(oaddr, swz)
+    if stats is not None:
+        _bank_stats(stats, "final_sts32", ophys, 4)
+    obuf = np.zeros(E, np.uint32)
+    obuf[ophys // 4] = words
+    assert len(np.unique(ophys)) == ophys.size, "output staging addresses collide"
+    return obuf[_swz(lin, swz) // 4]
+
+
+def _bank_stats(stats, name, addrs, width):
+    """addrs: (..., 128 lanes, n_instr) byte addresses of one access each.
+    Counts shared-memory wavefronts per warp instruction."""
+    a = np.asarray(addrs)
+    a = a.reshape(-1, 128, a.shape[-1]) if a.ndim >= 3 else a.reshape(1, 128, -1)
+    lanes_per_phase = 32 if width <= 4 else (16 if width == 8 else 8)
+    tot = cnt = 0
+    for tile in a:
+        for w in range(4):
+            warp = tile[32 * w: 32 * w + 32]
+            for ins in range(warp.shape[1]):
+                wf = 0
+                for p0 in range(0, 32, lanes_per_phase):
+                    words = set()
+                    for lane in range(p0, p0 + lanes_per_phase):
+                        for b in range(0, width, 4):
+                            words.add(int(warp[lane, ins]) + b)
+                    banks = {}
+                    for x in words:
+                        banks.setdefault((x // 4) % 32, set()).add(x // 4)
+                    wf += max(len(v) for v in banks.values())
+                tot += wf
+                cnt += 1
+    ideal = 1 if width <= 4 else (2 if width == 8 else 4)
+    s = stats.setdefault(name, [0, 0, ideal])
+    s[0] += tot
+    s[1] += cnt
+
+
+def run_pass_row(pt: PassTables, pairs: np.ndarray, stats=None) -> np.ndarray:
+    """pairs: (count, N, 2) fp16 contiguous transforms."""
+    N, T, E = pt.d["N"], pt.d["T"], pt.d["E"]
+    count = pairs.shape[0]
+    words = np.ascontiguousarray(pairs).view(np.uint32).reshape(-1)
+    out = np.empty_like(words)
+    for c in range(0, count, T):
+        w = np.zeros(E, np.uint32)
+        seg = words[c * N: min(count, c + T) * N]
+        w[: seg.size] = seg
+        o = emulate_chunk(pt, w, stats if c == 0 else None)
+        out[c * N: c * N + seg.size] = o[: seg.size]
+    return out.view(np.float16).reshape(pairs.shape)
+
+
+def run_pass_strip(pt: PassTables, img: np.ndarray, stats=None) -> np.ndarray:
+    """img: (images, nx, ny, 2) fp16; column FFTs of length nx."""
+    d = pt.d
+    C, IMG = d["C"], d["IMG"]
+    B, nx, ny, _ = img.shape
+    words = np.ascontiguousarray(img).view(np.uint32)[..., 0]  # (B, nx, ny)
+    out = np.empty_like(words)
+    first = True
+    for b0 in range(0, B, IMG):
+        for c0 in range(0, ny, C):
+            blk = np.zeros((IMG, nx, C), np.uint32)
+            nb = min(IMG, B - b0)
+            blk[:nb] = words[b0: b0 + nb, :, c0: c0 + C]
+            o = emulate_chunk(pt, blk.reshape(-1), stats if first else None).reshape(IMG, nx, C)
+            first = False
+            out[b0: b0 + nb, :, c0: c0 + C] = o[:nb]
+    return out[..., None].view(np.float16).reshape(img.shape)
