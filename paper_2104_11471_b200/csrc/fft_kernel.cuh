@@ -27,20 +27,29 @@
 
 namespace tcfft {
 
+// One side (load or store) of a pass, see plan.hpp IoDesc.
+struct KIo {
+  int32_t mode;         // IoMode
+  int32_t box_rows, n_sub, sub_bytes, chunk_rows;
+  int32_t C, spi;       // box: columns per chunk, chunks per image
+  int32_t pitch_bytes;  // pitch mode: staging pitch per transform
+  int64_t count;        // pitch mode: transforms in the pass
+  const uint8_t* gptr;  // pitch mode: raw global pointer, set per execution
+};
+
 struct KParams {
   int64_t chunks;
-  int32_t flat;            // 2: contiguous, rank-1 map; 1: contiguous, [total/W][W] map; 0: 3D column box
-  int32_t chunk_rows;      // flat: rows of the flat view per chunk (E / W)
-  int32_t strips_per_image;
-  int32_t C;               // box: columns per strip
-  int32_t gstride, ostride, swz;
+  int32_t T;  // transforms per chunk
+  int32_t gstride, ostride, swz_in, swz_out;
   int32_t tiles_max;
-  int32_t box_rows, n_sub;  // TMA sub-boxes per chunk (256-row limit)
-  int32_t sub_bytes;
+  KIo in, out;
   const RowInfo* rows_tab;
   const uint16_t* bblob;
   int32_t bbytes;
-  int32_t smem_a, smem_b, smem_bar;
+  int32_t smem_a, smem_b, smem_bar, smem_tw4;
+  int64_t tw4_total;  // four-step pass 1: full transform length
+  int32_t tw4_nk;     // number of final-stage k values (N1 / R_S)
+  int32_t tw4_s;      // N1 / R_S
 };
 
 namespace dev {
@@ -48,10 +57,13 @@ namespace dev {
 using namespace sm100;
 
 // ---------------------------------------------------------------- compile-time pass geometry
-template <int E_, int R1_, int R2_, int R3_, bool ROW_>
+enum : int { kModeRow = 0, kModeStrip = 1, kModeRowT = 2 };
+
+template <int E_, int R1_, int R2_, int R3_, int MODE_>
 struct Cfg {
   static constexpr int E = E_;
-  static constexpr bool ROW = ROW_;
+  static constexpr bool ROW_IN = MODE_ != kModeStrip;   // contiguous rows in (compile-time strides)
+  static constexpr bool ROW = MODE_ == kModeRow;        // ... and contiguous rows out
   static constexpr int S = (R2_ == 0) ? 1 : ((R3_ == 0) ? 2 : 3);
   static constexpr int N = R1_ * (R2_ ? R2_ : 1) * (R3_ ? R3_ : 1);
   __host__ __device__ static constexpr int R(int s) { return s == 0 ? R1_ : (s == 1 ? R2_ : R3_); }
@@ -69,8 +81,11 @@ struct Cfg {
   // staging strides (words) and swizzle, compile-time for contiguous row passes
   static constexpr int GS = N / R(0);
   static constexpr int OS = N / RL;
-  static constexpr uint32_t SWZ = (N >= 32) ? 0x70u : 0u;
-  static constexpr bool AFF_IN = ROW && (SWZ == 0 || (GS * 4) % 1024 == 0);
+  // row passes: 128B-swizzled staging for N == 32 and N >= 2048; 64 <= N <= 1024
+  // use padded per-transform staging (plan.cpp pitch_mode) without swizzle
+  static constexpr bool PITCH = ROW_IN && N >= 64 && N <= 1024;
+  static constexpr uint32_t SWZ = (N >= 32 && !PITCH) ? 0x70u : 0u;
+  static constexpr bool AFF_IN = ROW_IN && (SWZ == 0 || (GS * 4) % 1024 == 0);
   static constexpr bool AFF_OUT = ROW && (SWZ == 0 || (OS * 4) % 1024 == 0);
   // TMEM: D region (max over stages) then the stage-1 A region
   __host__ __device__ static constexpr int DC(int s) { return T(s) * NP(s); }
@@ -122,8 +137,8 @@ DEVI void gather_to_tmem(uint32_t s_in, int gbase, int gstride, uint32_t swzmask
 #pragma unroll
     for (int m = 0; m < KC; ++m) v[m] = (m < R) ? lds32(b0 + m * C::GS * 4) : 0u;
   } else {
-    const int gs = C::ROW ? C::GS : gstride;
-    const uint32_t msk = C::ROW ? C::SWZ : swzmask;
+    const int gs = C::ROW_IN ? C::GS : gstride;
+    const uint32_t msk = C::ROW_IN ? C::SWZ : swzmask;
 #pragma unroll
     for (int m = 0; m < KC; ++m)
       v[m] = (m < R) ? lds32(s_in + swz((uint32_t)(gbase + m * gs) * 4u, msk)) : 0u;
@@ -160,6 +175,29 @@ DEVI void load_group(uint32_t taddr, int j0, float* xr, float* xi) {
   }
 }
 
+// Twiddle sequence t_j = c * w^j, advanced two outputs at a time (packed
+// FFMA2 on the pairs (t_j, t_{j+1})); exact values come from the host / the
+// per-chunk table, the recurrence adds ~R ulps of fp32 error.
+struct TwSeq {
+  float2 tr, ti, w2r, w2i;
+  DEVI TwSeq(float2 c, float2 w) {
+    const float2 w2 = make_float2(w.x * w.x - w.y * w.y, 2.f * w.x * w.y);
+    w2r = make_float2(w2.x, w2.x);
+    w2i = make_float2(w2.y, w2.y);
+    tr = make_float2(c.x, c.x * w.x - c.y * w.y);
+    ti = make_float2(c.y, c.x * w.y + c.y * w.x);
+  }
+  // y = x * t for the current pair, then advance
+  DEVI void apply(float2 xr, float2 xi, float2& yr, float2& yi) {
+    yr = ffma2(neg2(xi), ti, fmul2(xr, tr));  // xr*tr - xi*ti
+    yi = ffma2(xi, tr, fmul2(xr, ti));        // xr*ti + xi*tr
+    const float2 ntr = ffma2(neg2(ti), w2i, fmul2(tr, w2r));
+    const float2 nti = ffma2(ti, w2r, fmul2(tr, w2i));
+    tr = ntr;
+    ti = nti;
+  }
+};
+
 // Writer epilogue of stage s: y_j = x_j * c * w^j (fp32, packed pairs),
 // rounded once to fp16 split planes, 16B stores into stage s+1's MN-major A.
 // Processed in groups of (up to) 16 outputs to bound register pressure.
@@ -167,11 +205,7 @@ template <class C, int s>
 DEVI void writer_epilogue(uint32_t taddr, uint32_t dst, float2 c, float2 w) {
   constexpr int R = C::R(s);
   constexpr int G = R < 16 ? R : 16;
-  // pair (v_j, v_{j+1}) = (c w^j, c w^{j+1}); step w^2
-  const float2 w2 = make_float2(w.x * w.x - w.y * w.y, 2.f * w.x * w.y);
-  const float2 w2r = make_float2(w2.x, w2.x), w2i = make_float2(w2.y, w2.y);
-  float2 tr = make_float2(c.x, c.x * w.x - c.y * w.y);
-  float2 ti = make_float2(c.y, c.x * w.y + c.y * w.x);
+  TwSeq tw(c, w);
 #pragma unroll
   for (int g = 0; g < R / G; ++g) {
     float xr[G], xi[G];
@@ -182,16 +216,10 @@ DEVI void writer_epilogue(uint32_t taddr, uint32_t dst, float2 c, float2 w) {
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const int j = 8 * h + 2 * q;
-        const float2 a = make_float2(xr[j], xr[j + 1]);
-        const float2 b = make_float2(xi[j], xi[j + 1]);
-        const float2 yr = ffma2(neg2(b), ti, fmul2(a, tr));  // xr*tr - xi*ti
-        const float2 yi = ffma2(b, tr, fmul2(a, ti));        // xr*ti + xi*tr
+        float2 yr, yi;
+        tw.apply(make_float2(xr[j], xr[j + 1]), make_float2(xi[j], xi[j + 1]), yr, yi);
         pr[q] = pack_half2(yr.x, yr.y);
         pi[q] = pack_half2(yi.x, yi.y);
-        const float2 ntr = ffma2(neg2(ti), w2i, fmul2(tr, w2r));
-        const float2 nti = ffma2(ti, w2r, fmul2(tr, w2i));
-        tr = ntr;
-        ti = nti;
       }
       const uint32_t d = dst + ((g * G) / 8 + h) * C::HSTEP(s);
       sts128(d, pr[0], pr[1], pr[2], pr[3]);
@@ -200,65 +228,84 @@ DEVI void writer_epilogue(uint32_t taddr, uint32_t dst, float2 c, float2 w) {
   }
 }
 
-// Final epilogue: natural-order interleaved output into the staging tile.
-template <class C>
-DEVI void final_epilogue(uint32_t taddr, uint32_t s_out, int obase, int ostride, uint32_t swzmask) {
+// Final epilogue: natural-order interleaved output into the staging tile,
+// optionally times the four-step twiddle c4 * w4^j.
+template <class C, bool TW4>
+DEVI void final_epilogue(uint32_t taddr, uint32_t s_out, int obase, int ostride, uint32_t swzmask, float2 c4,
+                         float2 w4) {
   constexpr int R = C::RL;
   constexpr int G = R < 16 ? R : 16;
   const int os = C::ROW ? C::OS : ostride;
   const uint32_t msk = C::ROW ? C::SWZ : swzmask;
   const uint32_t b0 = s_out + swz((uint32_t)obase * 4u, C::SWZ);
+  TwSeq tw(c4, w4);
 #pragma unroll
   for (int g = 0; g < R / G; ++g) {
     float xr[G], xi[G];
     load_group<R, G>(taddr, g * G, xr, xi);
 #pragma unroll
-    for (int jj = 0; jj < G; ++jj) {
-      const int j = g * G + jj;
-      const uint32_t wv = pack_half2(xr[jj], xi[jj]);
-      if constexpr (C::AFF_OUT)
-        sts32(b0 + j * C::OS * 4, wv);
-      else
-        sts32(s_out + swz((uint32_t)(obase + j * os) * 4u, msk), wv);
+    for (int jp = 0; jp < G / 2; ++jp) {
+      float2 yr = make_float2(xr[2 * jp], xr[2 * jp + 1]);
+      float2 yi = make_float2(xi[2 * jp], xi[2 * jp + 1]);
+      if constexpr (TW4) tw.apply(make_float2(xr[2 * jp], xr[2 * jp + 1]), make_float2(xi[2 * jp], xi[2 * jp + 1]), yr, yi);
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int j = g * G + 2 * jp + e;
+        const uint32_t wv = e ? pack_half2(yr.y, yi.y) : pack_half2(yr.x, yi.x);
+        if constexpr (C::AFF_OUT)
+          sts32(b0 + j * C::OS * 4, wv);
+        else
+          sts32(s_out + swz((uint32_t)(obase + j * os) * 4u, msk), wv);
+      }
     }
   }
 }
 
-DEVI void issue_load(const CUtensorMap* tm, const KParams& p, int64_t chunk, uint8_t* dst, uint64_t* bar) {
-  mbar_arrive_expect_tx(bar, (uint32_t)(p.n_sub * p.sub_bytes));
-  if (p.flat == 2) {
-    int32_t e0 = (int32_t)(chunk * p.chunk_rows);
-    for (int i = 0; i < p.n_sub; ++i) tma_load_1d(dst + i * p.sub_bytes, tm, e0 + i * p.box_rows, bar);
-  } else if (p.flat) {
-    int32_t row0 = (int32_t)(chunk * p.chunk_rows);
-    for (int i = 0; i < p.n_sub; ++i) tma_load_2d(dst + i * p.sub_bytes, tm, 0, row0 + i * p.box_rows, bar);
+DEVI void issue_load(const CUtensorMap* tm, const KIo& io, int T, int64_t chunk, uint8_t* dst, uint64_t* bar) {
+  if (io.mode == kIoPitch) {
+    const int64_t t0 = chunk * T;
+    const int nt = (int)min((int64_t)T, io.count - t0);
+    mbar_arrive_expect_tx(bar, (uint32_t)(nt * io.sub_bytes));
+    for (int i = 0; i < nt; ++i) bulk_g2s(dst + i * io.pitch_bytes, io.gptr + (t0 + i) * io.sub_bytes, io.sub_bytes, bar);
+    return;
+  }
+  mbar_arrive_expect_tx(bar, (uint32_t)(io.n_sub * io.sub_bytes));
+  if (io.mode == kIoRank1) {
+    const int32_t e0 = (int32_t)(chunk * io.chunk_rows);
+    for (int i = 0; i < io.n_sub; ++i) tma_load_1d(dst + i * io.sub_bytes, tm, e0 + i * io.box_rows, bar);
+  } else if (io.mode == kIoFlat) {
+    const int32_t row0 = (int32_t)(chunk * io.chunk_rows);
+    for (int i = 0; i < io.n_sub; ++i) tma_load_2d(dst + i * io.sub_bytes, tm, 0, row0 + i * io.box_rows, bar);
   } else {
-    int32_t img = (int32_t)(chunk / p.strips_per_image);
-    int32_t cb = (int32_t)(chunk % p.strips_per_image);
-    for (int i = 0; i < p.n_sub; ++i) {
+    const int32_t img = (int32_t)(chunk / io.spi), cb = (int32_t)(chunk % io.spi);
+    for (int i = 0; i < io.n_sub; ++i) {
       asm volatile(
           "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
-          "%4}], [%5];" ::"r"(smem_u32(dst + i * p.sub_bytes)),
-          "l"(tm), "r"(cb * p.C), "r"(i * p.box_rows), "r"(img), "r"(smem_u32(bar))
+          "%4}], [%5];" ::"r"(smem_u32(dst + i * io.sub_bytes)),
+          "l"(tm), "r"(cb * io.C), "r"(i * io.box_rows), "r"(img), "r"(smem_u32(bar))
           : "memory");
     }
   }
 }
 
-DEVI void issue_store(const CUtensorMap* tm, const KParams& p, int64_t chunk, const uint8_t* src) {
-  if (p.flat == 2) {
-    int32_t e0 = (int32_t)(chunk * p.chunk_rows);
-    for (int i = 0; i < p.n_sub; ++i) tma_store_1d(tm, e0 + i * p.box_rows, src + i * p.sub_bytes);
-  } else if (p.flat) {
-    int32_t row0 = (int32_t)(chunk * p.chunk_rows);
-    for (int i = 0; i < p.n_sub; ++i) tma_store_2d(tm, 0, row0 + i * p.box_rows, src + i * p.sub_bytes);
+DEVI void issue_store(const CUtensorMap* tm, const KIo& io, int T, int64_t chunk, const uint8_t* src) {
+  if (io.mode == kIoPitch) {
+    const int64_t t0 = chunk * T;
+    const int nt = (int)min((int64_t)T, io.count - t0);
+    for (int i = 0; i < nt; ++i)
+      bulk_s2g(const_cast<uint8_t*>(io.gptr) + (t0 + i) * io.sub_bytes, src + i * io.pitch_bytes, io.sub_bytes);
+  } else if (io.mode == kIoRank1) {
+    const int32_t e0 = (int32_t)(chunk * io.chunk_rows);
+    for (int i = 0; i < io.n_sub; ++i) tma_store_1d(tm, e0 + i * io.box_rows, src + i * io.sub_bytes);
+  } else if (io.mode == kIoFlat) {
+    const int32_t row0 = (int32_t)(chunk * io.chunk_rows);
+    for (int i = 0; i < io.n_sub; ++i) tma_store_2d(tm, 0, row0 + i * io.box_rows, src + i * io.sub_bytes);
   } else {
-    int32_t img = (int32_t)(chunk / p.strips_per_image);
-    int32_t cb = (int32_t)(chunk % p.strips_per_image);
-    for (int i = 0; i < p.n_sub; ++i) {
+    const int32_t img = (int32_t)(chunk / io.spi), cb = (int32_t)(chunk % io.spi);
+    for (int i = 0; i < io.n_sub; ++i) {
       asm volatile(
           "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(tm),
-          "r"(cb * p.C), "r"(i * p.box_rows), "r"(img), "r"(smem_u32(src + i * p.sub_bytes))
+          "r"(cb * io.C), "r"(i * io.box_rows), "r"(img), "r"(smem_u32(src + i * io.sub_bytes))
           : "memory");
     }
   }
@@ -290,12 +337,12 @@ DEVI void issue_stage_mma(uint32_t s_a, uint32_t s_b, uint32_t tD, uint32_t tA) 
 
 }  // namespace dev
 
-template <int E, int R1, int R2, int R3, int MINB, bool ROW>
+template <int E, int R1, int R2, int R3, int MINB, int MODE, bool TW4>
 __global__ void __launch_bounds__(128, MINB)
     fft_pass_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ CUtensorMap tm_out,
                     const KParams p) {
   using namespace dev;
-  using C = Cfg<E, R1, R2, R3, ROW>;
+  using C = Cfg<E, R1, R2, R3, MODE>;
   constexpr int S = C::S;
   constexpr int TM = C::TMAX;
 
@@ -325,6 +372,7 @@ __global__ void __launch_bounds__(128, MINB)
   auto rec = [&](int s, int t) -> const RowInfo& { return p.rows_tab[((size_t)s * p.tiles_max + t) * 128 + tid]; };
   // stage-0 writers have c = 1; the final stage needs only its output address
   int gb[C::T(0)];
+  int fk[TW4 ? C::T(S - 1) : 1];
   int waddr[S][TM];
   float2 wc[S][TM], ww[S][TM];
 #pragma unroll
@@ -336,8 +384,9 @@ __global__ void __launch_bounds__(128, MINB)
       if (t < C::T(s)) {
         const RowInfo& r = rec(s, t);
         waddr[s][t] = r.addr;
-        if (s + 1 < S) ww[s][t] = make_float2(r.wr, r.wi);
-        if (s >= 1 && s + 1 < S) wc[s][t] = make_float2(r.cr, r.ci);
+        if (s + 1 < S || TW4) ww[s][t] = make_float2(r.wr, r.wi);
+        if ((s >= 1 && s + 1 < S) || (TW4 && s + 1 == S)) wc[s][t] = make_float2(r.cr, r.ci);
+        if (TW4 && s + 1 == S) fk[t] = r.mp;
       }
     }
 
@@ -350,24 +399,36 @@ __global__ void __launch_bounds__(128, MINB)
   const uint32_t tD = tbase;
   const uint32_t tA = tbase + (uint32_t)C::DCOLS;
 
+  float2* s_tw4 = reinterpret_cast<float2*>(smem + p.smem_tw4);
+
   int64_t chunk = blockIdx.x;
-  if (tid == 0 && chunk < p.chunks) issue_load(&tm_in, p, chunk, s_in, &bars[0]);
+  if (tid == 0 && chunk < p.chunks) issue_load(&tm_in, p.in, p.T, chunk, s_in, &bars[0]);
   uint32_t ld_phase = 0, mma_phase = 0;
 
   for (; chunk < p.chunks; chunk += gridDim.x) {
+    if constexpr (TW4) {
+      // four-step twiddle, strip-base part: A[k] = W_Ntot^{base k}, r = W_Ntot^{base s}
+      const int64_t base = (chunk % p.in.spi) * (int64_t)p.in.C;
+      for (int kk = tid; kk <= p.tw4_nk; kk += 128) {
+        const int64_t e = (base * (kk < p.tw4_nk ? kk : p.tw4_s)) % p.tw4_total;
+        float sn, cs;
+        sincospif(-2.0f * (float)e / (float)p.tw4_total, &sn, &cs);
+        s_tw4[kk] = make_float2(cs, sn);
+      }
+    }
     mbar_wait(&bars[0], ld_phase);
     ld_phase ^= 1;
     // ---------------- stage 1: gather -> TMEM A
 #pragma unroll
     for (int t = 0; t < C::T(0); ++t)
-      gather_to_tmem<C>(s_in_u, gb[t], p.gstride, (uint32_t)p.swz, tA + lane_off + t * (C::KP(0) / 2));
+      gather_to_tmem<C>(s_in_u, gb[t], p.gstride, (uint32_t)p.swz_in, tA + lane_off + t * (C::KP(0) / 2));
     tmem_wait_st();
     tc_fence_before();
     __syncthreads();
     if (tid == 0) {
       tc_fence_after();
       int64_t nxt = chunk + gridDim.x;
-      if (nxt < p.chunks) issue_load(&tm_in, p, nxt, s_in, &bars[0]);  // staging buffer is free again
+      if (nxt < p.chunks) issue_load(&tm_in, p.in, p.T, nxt, s_in, &bars[0]);  // staging buffer is free again
       bulk_wait_read0();  // previous chunk's output store no longer reads s_a
       issue_stage_mma<C, 0>(s_a_u, s_b_u, tD, tA);
       mma_commit(&bars[1]);
@@ -399,12 +460,20 @@ __global__ void __launch_bounds__(128, MINB)
     if constexpr (S >= 3) writer(std::integral_constant<int, 1>{});
     // ---------------- final epilogue -> output staging (reuses s_a)
 #pragma unroll
-    for (int t = 0; t < C::T(S - 1); ++t)
-      final_epilogue<C>(tD + lane_off + t * C::NP(S - 1), s_a_u, waddr[S - 1][t], p.ostride, (uint32_t)p.swz);
+    for (int t = 0; t < C::T(S - 1); ++t) {
+      float2 c4 = make_float2(1.f, 0.f), w4 = make_float2(1.f, 0.f);
+      if constexpr (TW4) {
+        const float2 a = s_tw4[fk[t]], r = s_tw4[p.tw4_nk], hc = wc[S - 1][t], hw = ww[S - 1][t];
+        c4 = make_float2(a.x * hc.x - a.y * hc.y, a.x * hc.y + a.y * hc.x);
+        w4 = make_float2(r.x * hw.x - r.y * hw.y, r.x * hw.y + r.y * hw.x);
+      }
+      final_epilogue<C, TW4>(tD + lane_off + t * C::NP(S - 1), s_a_u, waddr[S - 1][t], p.ostride,
+                             (uint32_t)p.swz_out, c4, w4);
+    }
     fence_proxy_async_smem();
     tc_fence_before();
     __syncthreads();
-    if (tid == 0) issue_store(&tm_out, p, chunk, s_a);
+    if (tid == 0) issue_store(&tm_out, p.out, p.T, chunk, s_a);
   }
   if (tid == 0) bulk_wait0();
   tc_fence_before();

@@ -12,6 +12,7 @@
 
 #include <cmath>
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <tuple>
@@ -77,6 +78,13 @@ struct Bf {
 
 }  // namespace
 
+int pitch_pad_words(int n) {
+  // chosen with tests/emulator.py's bank model (see test_plan_emulation.py)
+  const char* e = std::getenv("TCFFT_PITCH_PAD");
+  if (e) return std::atoi(e);
+  return (n >= 64 && n <= 1024) ? 8 : 0;
+}
+
 std::vector<int> choose_radices(int n) {
   switch (n) {
     case 2: return {2};
@@ -104,7 +112,38 @@ int chunk_elems_for(int n) {
   return n;  // 8192, 16384: one transform per chunk
 }
 
-bool build_pass(PassPlan& p, int kind, int N, int64_t count, int64_t images, int cols, std::string* err) {
+// Flat (contiguous chunk) TMA view of `total` elements.
+static void flat_io(IoDesc& io, int64_t total, int E, bool allow_swizzle) {
+  // W = 32: [total/32][32] view, 128B swizzle; W = 4: [total/4][4];
+  // W = 1: rank-1 view [total] in 256-element boxes (any total).
+  const bool can32 = (total % 32 == 0) && allow_swizzle;
+  io.W = can32 ? 32 : (total % 4 == 0 ? 4 : 1);
+  io.mode = io.W == 1 ? kIoRank1 : kIoFlat;
+  io.swz = io.W == 32 ? 0x70 : 0;
+  io.box_rows = std::min(E / io.W, 256);
+  io.n_sub = (E / io.W) / io.box_rows;
+  io.sub_bytes = io.box_rows * io.W * 4;
+  io.chunk_rows = E / io.W;
+  io.total = total;
+}
+
+// 3D column-box TMA view of an images x rows x cols array, C columns per chunk.
+static void box_io(IoDesc& io, int64_t images, int rows, int cols, int C) {
+  io.mode = kIoBox;
+  io.images = images;
+  io.rows = rows;
+  io.cols = cols;
+  io.C = C;
+  io.spi = cols / C;
+  const int run = C * 4;
+  io.swz = run == 128 ? 0x70 : run == 64 ? 0x30 : run == 32 ? 0x10 : 0;
+  io.box_rows = std::min(rows, 256);
+  io.n_sub = rows / io.box_rows;
+  io.sub_bytes = io.box_rows * C * 4;
+}
+
+bool build_pass(PassPlan& p, int kind, int N, int64_t count, int64_t images, int cols, std::string* err,
+                int64_t tw4_total) {
   std::vector<int> rad = choose_radices(N);
   if (rad.empty()) {
     if (err) *err = "no single-pass radix schedule for N=" + std::to_string(N);
@@ -114,11 +153,26 @@ bool build_pass(PassPlan& p, int kind, int N, int64_t count, int64_t images, int
   p.kind = kind;
   p.N = N;
   p.S = (int)rad.size();
+  p.tw4_total = tw4_total;
+  const bool row_in = kind == kPassRow || kind == kPassRowT;
   if (kind == kPassRow) {
     p.E = chunk_elems_for(N);
     p.T = p.E / N;
     p.count = count;
     p.chunks = (count + p.T - 1) / p.T;
+  } else if (kind == kPassRowT) {
+    // rows of an images x (count/images) x N array, output transposed into
+    // images x N x (count/images): >= 4 rows per chunk (>= 16 B output runs)
+    p.E = std::max(chunk_elems_for(N), 4 * N);
+    p.T = p.E / N;
+    p.count = count;
+    p.chunks = (count + p.T - 1) / p.T;
+    p.images = images;
+    p.cols = (int)(count / images);  // rows per image = output columns
+    if ((p.cols % p.T) != 0) {
+      if (err) *err = "transposed row pass: rows per image must be a multiple of the chunk";
+      return false;
+    }
   } else {
     // Column strips of an images x N x cols array: C columns of IMG images per
     // chunk, E = N * C * IMG = max(chunk_elems_for(N), 4 N) (C >= 4: >= 16 B runs).
@@ -148,35 +202,51 @@ bool build_pass(PassPlan& p, int kind, int N, int64_t count, int64_t images, int
     if (err) *err = "unsupported chunk size";
     return false;
   }
-  const bool row = kind == kPassRow;
-  auto w_addr = [&](int tr, int n) -> int32_t {
-    return row ? tr * NN + n : (tr / C) * NN * C + n * C + tr % C;
+  // Contiguous row inputs with 64 <= N <= 1024 stage each transform at a padded
+  // pitch (per-transform bulk copies) so that the lanes of a warp, which span
+  // several short transforms, fall into different shared-memory banks.
+  p.pitch_mode = row_in && N >= 64 && N <= 1024;
+  p.pitch = p.pitch_mode ? N + pitch_pad_words(N) : N;  // words
+  const int PW = p.pitch;
+  auto w_in = [&](int tr, int n) -> int32_t {
+    return row_in ? tr * PW + n : (tr / C) * NN * C + n * C + tr % C;
   };
-  p.gstride = (N / rad[0]) * (row ? 1 : C);
-  p.ostride = (N / rad[S - 1]) * (row ? 1 : C);
-  // Load mechanism: a contiguous chunk uses a flat 2D tensor map [total/W][W];
-  // a column strip (C < cols) uses a 3D box {C, rows, 1}.
-  int64_t total = row ? count * (int64_t)N : images * (int64_t)N * cols;
-  p.flat = row || p.C == cols;
-  if (p.flat) {
-    // W = 32: [total/32][32] view, 128B swizzle; W = 4: [total/4][4];
-    // W = 1: rank-1 view [total] in 256-element boxes (any total).
-    // (row passes with N < 32 stay unswizzled: the kernel's compile-time row
-    // addressing assumes the 128B swizzle exactly when N >= 32)
-    const bool can32 = (total % 32 == 0) && (!row || N >= 32);
-    p.W = can32 ? 32 : (total % 4 == 0 ? 4 : 1);
-    p.swz_in = p.swz_out = p.W == 32 ? 0x70 : 0;
-    p.box_rows = std::min(E / p.W, 256);
-    p.n_sub = (E / p.W) / p.box_rows;
-    p.sub_bytes = p.box_rows * p.W * 4;
+  auto w_out = [&](int tr, int n) -> int32_t {
+    if (kind == kPassRow) return tr * PW + n;
+    if (kind == kPassRowT) return n * T + tr;
+    return (tr / C) * NN * C + n * C + tr % C;
+  };
+  p.gstride = (N / rad[0]) * (row_in ? 1 : C);
+  p.ostride = (N / rad[S - 1]) * (kind == kPassRow ? 1 : (kind == kPassRowT ? T : C));
+
+  // ---- TMA / bulk-copy descriptors
+  if (row_in) {
+    const int64_t total = count * (int64_t)N;
+    if (p.pitch_mode) {
+      p.in.mode = kIoPitch;
+      p.in.swz = 0;
+      p.in.n_sub = T;
+      p.in.sub_bytes = N * 4;
+      p.in.total = total;
+    } else {
+      // row passes with N < 32 stay unswizzled: the kernel's compile-time row
+      // addressing assumes the 128B swizzle exactly when N == 32 or N >= 2048
+      flat_io(p.in, total, E, N >= 32);
+    }
+  } else if (p.C == cols) {
+    flat_io(p.in, images * (int64_t)N * cols, E, true);
   } else {
-    int run = C * 4;
-    p.swz_in = p.swz_out = run == 128 ? 0x70 : run == 64 ? 0x30 : run == 32 ? 0x10 : 0;
-    p.box_rows = std::min(N, 256);
-    p.n_sub = N / p.box_rows;
-    p.sub_bytes = p.box_rows * C * 4;
+    box_io(p.in, images, N, cols, C);
   }
-  p.total = total;
+  if (kind == kPassRowT) {
+    box_io(p.out, images, N, p.cols, T);
+  } else {
+    p.out = p.in;
+  }
+  p.swz_in = p.in.swz;
+  p.swz_out = p.out.swz;
+  p.flat = p.in.mode != kIoBox;
+  p.total = p.in.total;
 
   int n2 = 1, tiles_max = 0;
   for (int s = 0; s < S; ++s) {
@@ -230,11 +300,11 @@ bool build_pass(PassPlan& p, int kind, int N, int64_t count, int64_t images, int
   {
     std::vector<std::tuple<int32_t, int, int>> order;
     for (int tr = 0; tr < T; ++tr)
-      for (int blk = 0; blk < N / R1; ++blk) order.emplace_back(w_addr(tr, bnat(blk)), tr, blk);
+      for (int blk = 0; blk < N / R1; ++blk) order.emplace_back(w_in(tr, bnat(blk)), tr, blk);
     std::sort(order.begin(), order.end());
     for (auto& o : order) cur.push_back(Bf{std::get<1>(o), 0, std::get<2>(o)});
   }
-  for (size_t i = 0; i < cur.size(); ++i) rec(0, (int)i).gbase = w_addr(cur[i].tr, bnat(cur[i].blk));
+  for (size_t i = 0; i < cur.size(); ++i) rec(0, (int)i).gbase = w_in(cur[i].tr, bnat(cur[i].blk));
 
   for (int s = 0; s + 1 < S; ++s) {
     StageInfo& st = p.st[s];
@@ -275,7 +345,24 @@ bool build_pass(PassPlan& p, int kind, int N, int64_t count, int64_t images, int
     }
     cur.swap(nxt);
   }
-  for (size_t i = 0; i < cur.size(); ++i) rec(S - 1, (int)i).addr = w_addr(cur[i].tr, cur[i].k);
+  for (size_t i = 0; i < cur.size(); ++i) {
+    RowInfo& r = rec(S - 1, (int)i);
+    r.addr = w_out(cur[i].tr, cur[i].k);
+    if (tw4_total) {
+      // four-step twiddle W_Ntot^{n2 k1}, n2 = strip base + tr, k1 = k + (N/R_S) j:
+      // host part W^{tr k} * (W^{tr s})^j, s = N/R_S; the strip-base part is
+      // rebuilt per chunk on the device (kernel tw4 tables).
+      const int64_t s_ = N / rad[S - 1];
+      double cr, ci, wr, wi;
+      root((int64_t)cur[i].tr * cur[i].k, tw4_total, &cr, &ci);
+      root((int64_t)cur[i].tr * s_, tw4_total, &wr, &wi);
+      r.mp = cur[i].k;
+      r.cr = (float)cr;
+      r.ci = (float)ci;
+      r.wr = (float)wr;
+      r.wi = (float)wi;
+    }
+  }
 
   // ---- B matrices ---------------------------------------------------------
   p.bblob.clear();
@@ -316,16 +403,19 @@ bool build_pass(PassPlan& p, int kind, int N, int64_t count, int64_t images, int
   p.tblob.clear();  // twiddles come from the per-row (c, w) recurrence
 
   // ---- shared memory / TMEM budget ---------------------------------------
-  int a_bytes = E * 4;
+  const int stage_bytes = row_in ? T * PW * 4 : E * 4;
+  const int tw4_bytes = tw4_total ? ((N / rad[S - 1]) * 8 + 16 + 127) & ~127 : 0;
+  int a_bytes = stage_bytes;
   for (int s = 1; s < S; ++s) a_bytes = std::max(a_bytes, p.st[s].tiles * p.st[s].tile_bytes);
   a_bytes = (a_bytes + 1023) & ~1023;
   p.a_bytes = a_bytes;
   p.smem_in = 0;
-  p.smem_a = E * 4;
+  p.smem_a = (stage_bytes + 1023) & ~1023;
   p.smem_b = p.smem_a + a_bytes;
   int bsz = ((int)p.bblob.size() * 2 + 127) & ~127;
   p.smem_t = p.smem_b + bsz;
-  p.smem_bar = p.smem_t;
+  p.smem_tw4 = p.smem_t;
+  p.smem_bar = p.smem_tw4 + tw4_bytes;
   p.smem_bytes = p.smem_bar + 64 /*mbarriers + TMEM address*/ + 1024 /*alignment slack*/;
   int acols = p.st[0].tiles * (p.st[0].KP / 2);
   int dcols = 0;
@@ -359,10 +449,32 @@ int build_plan(Plan& plan, int dims, int nx, int ny, int64_t batch, std::string*
     if (err) *err = "batch must be >= 1";
     return 3;  // TCFFT_INVALID_VALUE
   }
-  if (dims == 1) {
+  if (dims == 1 && nx <= 16384) {
     PassPlan p;
     if (!build_pass(p, kPassRow, nx, batch, 0, 0, err)) return 6;  // NOT_SUPPORTED
     plan.passes.push_back(std::move(p));
+    return 0;
+  }
+  if (dims == 1) {
+    // Four-step, N = N1 * N2 viewed as [N1][N2] (reference plan.py:35-44 chains
+    // radix-8192 kernels instead; SPEC.md:452 leaves the schedule free):
+    //   pass 1: length-N1 column FFTs, twiddle W_N^{n2 k1}, -> workspace
+    //   pass 2: length-N2 row FFTs, transposed store X[k1 + N1 k2] -> output
+    int lg = 0;
+    while ((1 << lg) < nx) ++lg;
+    if (lg > 24) {
+      if (err) *err = "1D sizes above 2^24 are not supported";
+      return 6;
+    }
+    const int N1 = 1 << (lg / 2), N2 = 1 << (lg - lg / 2);
+    PassPlan p1, p2;
+    if (!build_pass(p1, kPassStrip, N1, 0, batch, N2, err, nx)) return 6;
+    if (!build_pass(p2, kPassRowT, N2, batch * (int64_t)N1, batch, 0, err)) return 6;
+    p1.ws_out = 1;
+    p2.ws_in = 1;
+    plan.ws_bytes = (size_t)batch * (size_t)nx * 4;
+    plan.passes.push_back(std::move(p1));
+    plan.passes.push_back(std::move(p2));
     return 0;
   }
   // 2D, row-major (nx, ny): contiguous rows (ny) first, then columns (nx)

@@ -20,7 +20,26 @@ constexpr int kLanes = 128;  // M of every tcgen05.mma tile
 
 enum PassKind : int32_t {
   kPassRow = 0,    // contiguous transforms: element n of transform tr at tr*N + n
-  kPassStrip = 1,  // column strip: element n of column tr at n*C + tr (2D column pass)
+  kPassStrip = 1,  // column strip: element n of column tr at n*C + tr (2D column / four-step pass 1)
+  kPassRowT = 2,   // contiguous rows in, transposed columns out (four-step pass 2)
+};
+
+enum IoMode : int32_t {
+  kIoBox = 0,    // 3D tensor map {C, rows, 1} over images x rows x cols
+  kIoFlat = 1,   // 2D tensor map [total/W][W] over a contiguous chunk
+  kIoRank1 = 2,  // 1D tensor map [total] in 256-element boxes
+  kIoPitch = 3,  // per-transform 1D bulk copies into a padded staging pitch
+};
+
+// How one side (load or store) of a pass moves a chunk between HBM and SMEM.
+struct IoDesc {
+  int32_t mode = kIoFlat;
+  int32_t W = 0, swz = 0;
+  int32_t box_rows = 0, n_sub = 0, sub_bytes = 0, chunk_rows = 0;
+  int32_t C = 0, spi = 0;  // box: columns per chunk, chunks per image
+  int64_t images = 0;
+  int32_t rows = 0, cols = 0;
+  int64_t total = 0;
 };
 
 struct StageInfo {
@@ -66,6 +85,11 @@ struct PassPlan {
   int32_t rows, cols, C, IMG;
   // TMA: flat contiguous chunk ([total/W][W] view) or 3D column box
   int32_t flat, W, box_rows, n_sub, sub_bytes;
+  int32_t pitch_mode, pitch;  // row inputs, 64 <= N <= 1024: padded per-transform staging (words)
+  IoDesc in, out;
+  int64_t tw4_total;   // four-step pass 1: N of the full transform (extra twiddle), else 0
+  int32_t ws_in, ws_out;  // pass reads / writes the plan workspace
+  int32_t smem_tw4;
   int64_t total;
   // shared-memory carve-up (bytes, relative to the 1024-aligned base)
   int32_t smem_in, smem_a, smem_b, smem_t, smem_bar, smem_bytes;
@@ -83,15 +107,18 @@ struct Plan {
   int32_t dims = 1;
   int32_t nx = 0, ny = 0;
   int64_t batch = 0;
+  size_t ws_bytes = 0;
   std::vector<PassPlan> passes;
 };
 
 // Radix list chosen for a single-pass transform of length n (product == n).
 std::vector<int> choose_radices(int n);
 int chunk_elems_for(int n);
+int pitch_pad_words(int n);
 
 // Builds a pass.  kind/geometry as in PassPlan; returns false on unsupported size.
-bool build_pass(PassPlan& p, int kind, int N, int64_t count, int64_t images, int cols, std::string* err);
+bool build_pass(PassPlan& p, int kind, int N, int64_t count, int64_t images, int cols, std::string* err,
+                int64_t tw4_total = 0);
 // Builds the whole plan (host-only, no CUDA calls).
 int build_plan(Plan& plan, int dims, int nx, int ny, int64_t batch, std::string* err);
 

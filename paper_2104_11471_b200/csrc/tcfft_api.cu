@@ -22,41 +22,49 @@ namespace {
 using KernelFn = void (*)(CUtensorMap, CUtensorMap, KParams);
 
 struct KernelEntry {
-  int E, R1, R2, R3, row;
+  int E, R1, R2, R3, mode, tw4;
   const void* fn;
   void (*launch)(dim3, int, cudaStream_t, const CUtensorMap&, const CUtensorMap&, const KParams&);
 };
 
-template <int E, int R1, int R2, int R3, int MINB, bool ROW>
+template <int E, int R1, int R2, int R3, int MINB, int MODE, bool TW4>
 void launch_tpl(dim3 grid, int smem, cudaStream_t st, const CUtensorMap& a, const CUtensorMap& b,
                 const KParams& p) {
-  tcfft::fft_pass_kernel<E, R1, R2, R3, MINB, ROW><<<grid, 128, smem, st>>>(a, b, p);
+  tcfft::fft_pass_kernel<E, R1, R2, R3, MINB, MODE, TW4><<<grid, 128, smem, st>>>(a, b, p);
 }
 
-#define KENTRY(E, R1, R2, R3, MB, ROW)                                                                     \
-  {                                                                                                        \
-    E, R1, R2, R3, ROW, (const void*)&tcfft::fft_pass_kernel<E, R1, R2, R3, MB, ROW>,                     \
-        &launch_tpl<E, R1, R2, R3, MB, ROW>                                                                \
+#define KENTRY(E, R1, R2, R3, MB, MODE, TW)                                                               \
+  {                                                                                                       \
+    E, R1, R2, R3, MODE, TW, (const void*)&tcfft::fft_pass_kernel<E, R1, R2, R3, MB, MODE, TW>,           \
+        &launch_tpl<E, R1, R2, R3, MB, MODE, TW>                                                          \
   }
-#define KBOTH(E, R1, R2, R3, MB) KENTRY(E, R1, R2, R3, MB, true), KENTRY(E, R1, R2, R3, MB, false)
+#define KROW(E, R1, R2, R3, MB) KENTRY(E, R1, R2, R3, MB, 0, false)
+#define KSTRIP(E, R1, R2, R3, MB) KENTRY(E, R1, R2, R3, MB, 1, false)
+#define KBOTH(E, R1, R2, R3, MB) KROW(E, R1, R2, R3, MB), KSTRIP(E, R1, R2, R3, MB)
+#define KFOUR(E, R1, R2, R3, MB) KENTRY(E, R1, R2, R3, MB, 1, true), KENTRY(E, R1, R2, R3, MB, 2, false)
 
-// Every (chunk size, radix list) the planner can emit, for contiguous row
-// passes (compile-time strides) and column-strip passes.
+// Every (chunk size, radix list, mode) the planner can emit: contiguous row
+// passes, column-strip passes (2D), and the two four-step passes (strip +
+// twiddle, rows in / transposed out) for 1D sizes 2^15 .. 2^24.
 const KernelEntry kKernels[] = {
-    KBOTH(1024, 2, 0, 0, 4),     KBOTH(2048, 4, 0, 0, 4),     KBOTH(4096, 8, 0, 0, 4),
-    KBOTH(4096, 16, 0, 0, 4),    KBOTH(4096, 32, 0, 0, 4),    KBOTH(4096, 8, 8, 0, 4),
-    KBOTH(4096, 16, 8, 0, 4),    KBOTH(4096, 16, 16, 0, 4),   KBOTH(4096, 16, 32, 0, 4),
-    KBOTH(4096, 32, 32, 0, 4),   KBOTH(4096, 16, 16, 8, 4),   KBOTH(4096, 16, 16, 16, 4),
-    KENTRY(8192, 16, 16, 32, 2, true),   KENTRY(8192, 16, 16, 8, 2, false),
-    KENTRY(16384, 16, 32, 32, 1, true),  KENTRY(16384, 16, 16, 16, 1, false),
+    KBOTH(1024, 2, 0, 0, 4),      KBOTH(2048, 4, 0, 0, 4),      KBOTH(4096, 8, 0, 0, 4),
+    KBOTH(4096, 16, 0, 0, 4),     KBOTH(4096, 32, 0, 0, 4),     KBOTH(4096, 8, 8, 0, 4),
+    KBOTH(4096, 16, 8, 0, 4),     KBOTH(4096, 16, 16, 0, 4),    KBOTH(4096, 16, 32, 0, 4),
+    KBOTH(4096, 32, 32, 0, 4),    KBOTH(4096, 16, 16, 8, 4),    KBOTH(4096, 16, 16, 16, 4),
+    KROW(8192, 16, 16, 32, 2),    KSTRIP(8192, 16, 16, 8, 2),   KROW(16384, 16, 32, 32, 1),
+    KSTRIP(16384, 16, 16, 16, 1),
+    // four-step: N1 / N2 in {128 .. 4096}
+    KFOUR(4096, 16, 8, 0, 4),     KFOUR(4096, 16, 16, 0, 4),    KFOUR(4096, 16, 32, 0, 4),
+    KFOUR(4096, 32, 32, 0, 4),    KFOUR(8192, 16, 16, 8, 2),    KFOUR(16384, 16, 16, 16, 1),
 };
 
 const KernelEntry* find_kernel(const PassPlan& p) {
   int r[3] = {0, 0, 0};
   for (int s = 0; s < p.S; ++s) r[s] = p.st[s].R;
-  const int row = p.kind == tcfft::kPassRow ? 1 : 0;
+  const int mode = p.kind;  // kPassRow 0, kPassStrip 1, kPassRowT 2 == kernel modes
+  const int tw4 = p.tw4_total ? 1 : 0;
   for (const auto& k : kKernels)
-    if (k.E == p.E && k.R1 == r[0] && k.R2 == r[1] && k.R3 == r[2] && k.row == row) return &k;
+    if (k.E == p.E && k.R1 == r[0] && k.R2 == r[1] && k.R3 == r[2] && k.mode == mode && k.tw4 == tw4) return &k;
   return nullptr;
 }
 
@@ -85,6 +93,7 @@ struct DevPass {
 struct tcfftPlanImpl {
   tcfft::Plan plan;
   std::vector<DevPass> dev;
+  void* ws = nullptr;
   cudaStream_t stream = nullptr;
   int device = 0;
   int magic = 0x7cff7;
@@ -92,41 +101,57 @@ struct tcfftPlanImpl {
 
 namespace {
 
-tcfftResult make_tmap(CUtensorMap* tm, const PassPlan& p, const void* base) {
+tcfftResult make_tmap(CUtensorMap* tm, const tcfft::IoDesc& io, const void* base) {
+  std::memset(tm, 0, sizeof(*tm));
+  if (io.mode == tcfft::kIoPitch) return TCFFT_SUCCESS;  // raw bulk copies, no tensor map
   auto enc = encode_fn();
   if (!enc) return TCFFT_EXEC_FAILED;
   CUresult r;
-  if (p.flat && p.W == 1) {
-    cuuint64_t dims[1] = {(cuuint64_t)p.total};
+  if (io.mode == tcfft::kIoRank1) {
+    cuuint64_t dims[1] = {(cuuint64_t)io.total};
     cuuint64_t strides[1] = {0};
-    cuuint32_t box[1] = {(cuuint32_t)p.box_rows};
+    cuuint32_t box[1] = {(cuuint32_t)io.box_rows};
     cuuint32_t es[1] = {1};
     r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_UINT32, 1, const_cast<void*>(base), dims, strides, box, es,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  } else if (p.flat) {
-    cuuint64_t dims[2] = {(cuuint64_t)p.W, (cuuint64_t)(p.total / p.W)};
-    cuuint64_t strides[1] = {(cuuint64_t)p.W * 4};
-    cuuint32_t box[2] = {(cuuint32_t)p.W, (cuuint32_t)p.box_rows};
+  } else if (io.mode == tcfft::kIoFlat) {
+    cuuint64_t dims[2] = {(cuuint64_t)io.W, (cuuint64_t)(io.total / io.W)};
+    cuuint64_t strides[1] = {(cuuint64_t)io.W * 4};
+    cuuint32_t box[2] = {(cuuint32_t)io.W, (cuuint32_t)io.box_rows};
     cuuint32_t es[2] = {1, 1};
     r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<void*>(base), dims, strides, box, es,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, p.W == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, io.W == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   } else {
-    cuuint64_t dims[3] = {(cuuint64_t)p.cols, (cuuint64_t)p.rows, (cuuint64_t)p.images};
-    cuuint64_t strides[2] = {(cuuint64_t)p.cols * 4, (cuuint64_t)p.cols * p.rows * 4};
-    cuuint32_t box[3] = {(cuuint32_t)p.C, (cuuint32_t)p.box_rows, 1};
+    cuuint64_t dims[3] = {(cuuint64_t)io.cols, (cuuint64_t)io.rows, (cuuint64_t)io.images};
+    cuuint64_t strides[2] = {(cuuint64_t)io.cols * 4, (cuuint64_t)io.cols * io.rows * 4};
+    cuuint32_t box[3] = {(cuuint32_t)io.C, (cuuint32_t)io.box_rows, 1};
     cuuint32_t es[3] = {1, 1, 1};
-    int run = p.C * 4;
+    const int run = io.C * 4;
     CUtensorMapSwizzle sw = run == 128  ? CU_TENSOR_MAP_SWIZZLE_128B
                             : run == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
                             : run == 32 ? CU_TENSOR_MAP_SWIZZLE_32B
                                         : CU_TENSOR_MAP_SWIZZLE_NONE;
     r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, const_cast<void*>(base), dims, strides, box, es,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   }
   return r == CUDA_SUCCESS ? TCFFT_SUCCESS : TCFFT_EXEC_FAILED;
+}
+
+tcfft::KIo to_kio(const tcfft::IoDesc& io, const PassPlan& p) {
+  tcfft::KIo k;
+  std::memset(&k, 0, sizeof(k));
+  k.mode = io.mode;
+  k.box_rows = io.box_rows;
+  k.n_sub = io.n_sub;
+  k.sub_bytes = io.sub_bytes;
+  k.chunk_rows = io.chunk_rows;
+  k.C = io.C;
+  k.spi = io.spi;
+  k.pitch_bytes = p.pitch * 4;
+  k.count = p.count;
+  return k;
 }
 
 tcfftResult map_build_status(int st) {
@@ -186,30 +211,38 @@ tcfftResult create(tcfftHandle* out, int dims, int nx, int ny, int batch) {
     KParams& k = d.kp;
     std::memset(&k, 0, sizeof(k));
     k.chunks = p.chunks;
-    k.flat = p.flat ? (p.W == 1 ? 2 : 1) : 0;
-    k.chunk_rows = p.flat ? p.E / p.W : 0;
-    k.strips_per_image = p.flat ? 1 : p.cols / p.C;
-    k.C = p.C;
+    k.T = p.T;
     k.gstride = p.gstride;
     k.ostride = p.ostride;
-    k.swz = p.swz_in;
+    k.swz_in = p.swz_in;
+    k.swz_out = p.swz_out;
     k.tiles_max = p.tiles_max;
-    k.box_rows = p.box_rows;
-    k.n_sub = p.n_sub;
-    k.sub_bytes = p.sub_bytes;
+    k.in = to_kio(p.in, p);
+    k.out = to_kio(p.out, p);
     k.rows_tab = reinterpret_cast<const tcfft::RowInfo*>(base);
     k.bblob = reinterpret_cast<const uint16_t*>(base + rb_al);
     k.bbytes = (int)(p.bblob.size() * 2);  // multiple of 512
     k.smem_a = p.smem_a;
     k.smem_b = p.smem_b;
     k.smem_bar = p.smem_bar;
+    k.smem_tw4 = p.smem_tw4;
+    k.tw4_total = p.tw4_total;
+    k.tw4_s = p.N / p.st[p.S - 1].R;
+    k.tw4_nk = k.tw4_s;
     cudaFuncSetAttribute(d.k->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, p.smem_bytes);
     int64_t slots = (int64_t)prop.multiProcessorCount * p.ctas_per_sm;
     d.grid = (int)std::min<int64_t>(p.chunks, slots);
     h->dev.push_back(d);
   }
+  if (h->plan.ws_bytes && cudaMalloc(&h->ws, h->plan.ws_bytes) != cudaSuccess) {
+    cudaGetLastError();
+    for (auto& q : h->dev) cudaFree(q.tables);
+    delete h;
+    return TCFFT_ALLOC_FAILED;
+  }
   if (cudaGetLastError() != cudaSuccess) {
     for (auto& q : h->dev) cudaFree(q.tables);
+    if (h->ws) cudaFree(h->ws);
     delete h;
     return TCFFT_EXEC_FAILED;
   }
@@ -235,7 +268,7 @@ tcfftResult tcfftSetStream(tcfftHandle plan, void* stream) {
 tcfftResult tcfftGetWorkspaceSize(tcfftHandle plan, size_t* bytes) {
   if (!valid(plan)) return TCFFT_INVALID_PLAN;
   if (!bytes) return TCFFT_INVALID_VALUE;
-  *bytes = 0;
+  *bytes = plan->plan.ws_bytes;
   return TCFFT_SUCCESS;
 }
 
@@ -243,15 +276,21 @@ tcfftResult tcfftExecC2C(tcfftHandle plan, const void* idata, void* odata) {
   if (!valid(plan)) return TCFFT_INVALID_PLAN;
   if (!idata || !odata) return TCFFT_INVALID_VALUE;
   if ((reinterpret_cast<uintptr_t>(idata) | reinterpret_cast<uintptr_t>(odata)) & 15) return TCFFT_INVALID_VALUE;
+  const void* src = idata;
   for (size_t i = 0; i < plan->dev.size(); ++i) {
     const PassPlan& p = plan->plan.passes[i];
     const DevPass& d = plan->dev[i];
-    const void* src = (i == 0) ? idata : odata;
+    void* dst = p.ws_out ? plan->ws : odata;
+    if (p.ws_in) src = plan->ws;
     CUtensorMap tin, tout;
-    if (make_tmap(&tin, p, src) != TCFFT_SUCCESS || make_tmap(&tout, p, odata) != TCFFT_SUCCESS)
+    if (make_tmap(&tin, p.in, src) != TCFFT_SUCCESS || make_tmap(&tout, p.out, dst) != TCFFT_SUCCESS)
       return TCFFT_EXEC_FAILED;
-    d.k->launch(dim3(d.grid), p.smem_bytes, plan->stream, tin, tout, d.kp);
+    KParams kp = d.kp;
+    kp.in.gptr = static_cast<const uint8_t*>(src);
+    kp.out.gptr = static_cast<const uint8_t*>(dst);
+    d.k->launch(dim3(d.grid), p.smem_bytes, plan->stream, tin, tout, kp);
     if (cudaGetLastError() != cudaSuccess) return TCFFT_EXEC_FAILED;
+    src = dst;
   }
   return TCFFT_SUCCESS;
 }
@@ -259,6 +298,7 @@ tcfftResult tcfftExecC2C(tcfftHandle plan, const void* idata, void* odata) {
 tcfftResult tcfftDestroy(tcfftHandle plan) {
   if (!valid(plan)) return TCFFT_INVALID_PLAN;
   for (auto& q : plan->dev) cudaFree(q.tables);
+  if (plan->ws) cudaFree(plan->ws);
   plan->magic = 0;
   delete plan;
   return TCFFT_SUCCESS;
@@ -289,15 +329,20 @@ tcfftResult tcfftDescribePlan(int dims, int nx, int ny, int batch, char* json, s
     s = "{\"error\": \"" + err + "\"}";
   } else {
     s = "{\"dims\": " + std::to_string(dims) + ", \"nx\": " + std::to_string(nx) + ", \"ny\": " +
-        std::to_string(ny) + ", \"batch\": " + std::to_string(batch) + ", \"passes\": [";
+        std::to_string(ny) + ", \"batch\": " + std::to_string(batch) + ", \"ws_bytes\": " +
+        std::to_string(plan.ws_bytes) + ", \"passes\": [";
     for (size_t i = 0; i < plan.passes.size(); ++i) {
       const PassPlan& p = plan.passes[i];
       if (i) s += ", ";
-      s += "{\"kind\": \"" + std::string(p.kind == tcfft::kPassRow ? "row" : "strip") + "\", \"N\": " +
+      s += "{\"kind\": \"" + std::string(p.kind == tcfft::kPassRow ? "row" : (p.kind == tcfft::kPassStrip ? "strip" : "rowT")) + "\", \"N\": " +
            std::to_string(p.N) + ", \"E\": " + std::to_string(p.E) + ", \"T\": " + std::to_string(p.T) +
            ", \"C\": " + std::to_string(p.C) + ", \"IMG\": " + std::to_string(p.IMG) +
            ", \"chunks\": " + std::to_string(p.chunks) + ", \"flat\": " + std::to_string(p.flat) +
-           ", \"W\": " + std::to_string(p.W) + ", \"gstride\": " + std::to_string(p.gstride) +
+           ", \"W\": " + std::to_string(p.in.W) + ", \"pitch\": " + std::to_string(p.pitch) +
+           ", \"in_mode\": " + std::to_string(p.in.mode) + ", \"out_mode\": " + std::to_string(p.out.mode) +
+           ", \"swz_in\": " + std::to_string(p.swz_in) + ", \"swz_out\": " + std::to_string(p.swz_out) +
+           ", \"tw4_total\": " + std::to_string(p.tw4_total) + ", \"ws_in\": " + std::to_string(p.ws_in) +
+           ", \"ws_out\": " + std::to_string(p.ws_out) + ", \"out_cols\": " + std::to_string(p.cols) + ", \"gstride\": " + std::to_string(p.gstride) +
            ", \"ostride\": " + std::to_string(p.ostride) + ", \"swz\": " + std::to_string(p.swz_in) +
            ", \"smem_bytes\": " + std::to_string(p.smem_bytes) + ", \"smem_a\": " + std::to_string(p.smem_a) +
            ", \"a_bytes\": " + std::to_string(p.a_bytes) + ", \"tmem_cols\": " + std::to_string(p.tmem_cols) +

@@ -48,15 +48,18 @@ def _half(x):
         return np.asarray(x, dtype=np.float32).astype(np.float16)
 
 
-def emulate_chunk(pt: PassTables, chunk_words: np.ndarray, stats: dict | None = None) -> np.ndarray:
-    """chunk_words: (E,) uint32 interleaved fp16 pairs in linear staging order.
-    Returns the (E,) uint32 output staging in linear order."""
+def emulate_chunk(pt: PassTables, chunk_words: np.ndarray, stats: dict | None = None,
+                  tw4_base: int = 0) -> np.ndarray:
+    """chunk_words: (L,) uint32 interleaved fp16 pairs in linear staging order.
+    Returns the (L,) uint32 output staging in linear order.  tw4_base: first
+    global column of the strip (four-step pass 1 twiddle)."""
     d = pt.d
-    E, swz = d["E"], d["swz"]
+    swz, swz_out = d["swz_in"], d["swz_out"]
+    L = len(chunk_words)
     stages = d["stages"]
     S = len(stages)
-    lin = np.arange(E, dtype=np.int64) * 4
-    sbuf = np.zeros(E, np.uint32)
+    lin = np.arange(L, dtype=np.int64) * 4
+    sbuf = np.zeros(L, np.uint32)
     sbuf[_swz(lin, swz) // 4] = chunk_words
 
     # ---- stage 1 gather -> A (TMEM), interleaved K
@@ -114,16 +117,26 @@ def emulate_chunk(pt: PassTables, chunk_words: np.ndarray, stats: dict | None = 
     st = stages[S - 1]
     R, T = st["R"], st["tiles"]
     rec = pt.rows[S - 1, :T]
-    hr, hi = _half(D[..., :R]), _half(D[..., R: 2 * R])
+    yr, yi = D[..., :R].astype(np.float32), D[..., R: 2 * R].astype(np.float32)
+    if d["tw4_total"]:
+        # kernel: c4 = A[k] * W^{tr k} (host), w4 = r * W^{tr s} (host); A, r per chunk
+        Nt, s_ = d["tw4_total"], d["N"] // R
+        A = np.exp(-2j * np.pi * ((tw4_base * rec["mp"].astype(np.int64)) % Nt) / Nt)
+        r = np.exp(-2j * np.pi * ((tw4_base * s_) % Nt) / Nt)
+        c4 = A * (rec["cr"] + 1j * rec["ci"])
+        w4 = r * (rec["wr"] + 1j * rec["wi"])
+        tw = (c4[..., None] * w4[..., None] ** np.arange(R)).astype(np.complex64)
+        yr, yi = yr * tw.real - yi * tw.imag, yr * tw.imag + yi * tw.real
+    hr, hi = _half(yr), _half(yi)
     words = np.stack([hr, hi], -1).view(np.uint32)[..., 0]  # (T,128,R)
     oaddr = (rec["addr"][..., None].astype(np.int64) + np.arange(R) * d["ostride"]) * 4
-    ophys = _swz(oaddr, swz)
+    ophys = _swz(oaddr, swz_out)
     if stats is not None:
         _bank_stats(stats, "final_sts32", ophys, 4)
-    obuf = np.zeros(E, np.uint32)
+    obuf = np.zeros(L, np.uint32)
     obuf[ophys // 4] = words
     assert len(np.unique(ophys)) == ophys.size, "output staging addresses collide"
-    return obuf[_swz(lin, swz) // 4]
+    return obuf[_swz(lin, swz_out) // 4]
 
 
 def _bank_stats(stats, name, addrs, width):
@@ -157,16 +170,16 @@ def _bank_stats(stats, name, addrs, width):
 
 def run_pass_row(pt: PassTables, pairs: np.ndarray, stats=None) -> np.ndarray:
     """pairs: (count, N, 2) fp16 contiguous transforms."""
-    N, T, E = pt.d["N"], pt.d["T"], pt.d["E"]
+    N, T, E, P = pt.d["N"], pt.d["T"], pt.d["E"], pt.d["pitch"]
     count = pairs.shape[0]
-    words = np.ascontiguousarray(pairs).view(np.uint32).reshape(-1)
+    words = np.ascontiguousarray(pairs).view(np.uint32).reshape(count, N)
     out = np.empty_like(words)
     for c in range(0, count, T):
-        w = np.zeros(E, np.uint32)
-        seg = words[c * N: min(count, c + T) * N]
-        w[: seg.size] = seg
-        o = emulate_chunk(pt, w, stats if c == 0 else None)
-        out[c * N: c * N + seg.size] = o[: seg.size]
+        nt = min(T, count - c)
+        w = np.zeros((T, P), np.uint32)
+        w[:nt, :N] = words[c: c + nt]
+        o = emulate_chunk(pt, w.reshape(-1), stats if c == 0 else None).reshape(T, P)
+        out[c: c + nt] = o[:nt, :N]
     return out.view(np.float16).reshape(pairs.shape)
 
 
@@ -183,7 +196,35 @@ def run_pass_strip(pt: PassTables, img: np.ndarray, stats=None) -> np.ndarray:
             blk = np.zeros((IMG, nx, C), np.uint32)
             nb = min(IMG, B - b0)
             blk[:nb] = words[b0: b0 + nb, :, c0: c0 + C]
-            o = emulate_chunk(pt, blk.reshape(-1), stats if first else None).reshape(IMG, nx, C)
+            o = emulate_chunk(pt, blk.reshape(-1), stats if first else None, tw4_base=c0).reshape(IMG, nx, C)
             first = False
             out[b0: b0 + nb, :, c0: c0 + C] = o[:nb]
     return out[..., None].view(np.float16).reshape(img.shape)
+
+
+def run_pass_rowT(pt: PassTables, rows: np.ndarray, images: int) -> np.ndarray:
+    """Four-step pass 2: rows (images*N1, N2, 2) fp16 -> out (images, N2, N1, 2)
+    (row k1 of image b lands in column k1 of the transposed output)."""
+    N, T, P = pt.d["N"], pt.d["T"], pt.d["pitch"]
+    count = rows.shape[0]
+    n1 = count // images
+    words = np.ascontiguousarray(rows).view(np.uint32).reshape(count, N)
+    out = np.zeros((images, N, n1), np.uint32)
+    for c in range(0, count, T):
+        w = np.zeros((T, P), np.uint32)
+        w[:, :N] = words[c: c + T]
+        o = emulate_chunk(pt, w.reshape(-1))[: T * N].reshape(N, T)
+        b, k0 = c // n1, c % n1
+        out[b, :, k0: k0 + T] = o
+    return out[..., None].view(np.float16).reshape(images, N, n1, 2)
+
+
+def run_fourstep(n: int, pairs: np.ndarray) -> np.ndarray:
+    """Full four-step 1D transform (both passes) of (B, n, 2) fp16."""
+    B = pairs.shape[0]
+    p1 = PassTables(1, n, 0, B, 0)
+    p2 = PassTables(1, n, 0, B, 1)
+    n1, n2 = p1.d["N"], p2.d["N"]
+    y = run_pass_strip(p1, pairs.reshape(B, n1, n2, 2))
+    z = run_pass_rowT(p2, y.reshape(B * n1, n2, 2), B)
+    return z.reshape(B, n, 2)

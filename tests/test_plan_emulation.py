@@ -6,7 +6,7 @@ import numpy as np
 import pytest
 
 from oracle import restate as R
-from tests.emulator import PassTables, run_pass_row, run_pass_strip
+from tests.emulator import PassTables, run_fourstep, run_pass_row, run_pass_strip
 
 SIZES_1D = [2, 4, 8, 16, 32, 64, 128, 256, 512, 1024, 2048, 4096, 8192, 16384]
 
@@ -61,3 +61,12 @@ def test_bank_conflicts_report(capsys):
                 assert tot / cnt <= 4 * ideal, (k, tot / cnt)
     with capsys.disabled():
         print("\n" + "\n".join(lines))
+
+
+@pytest.mark.parametrize("n,batch", [(1 << 15, 2), (1 << 16, 1), (1 << 17, 1)])
+def test_fourstep_emulation_matches_fft(n, batch):
+    x = R.random_pairs([11, n], batch, n)
+    y = run_fourstep(n, x)
+    assert np.isfinite(R.to_complex(y)).all()
+    e64 = _errs(y, x, n)
+    assert e64 < 1.5e-3, e64
