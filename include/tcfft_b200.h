@@ -54,6 +54,13 @@ tcfftResult tcfftGetWorkspaceSize(tcfftHandle plan, size_t* bytes);
  * (interleaved complex), 16-byte aligned; odata may equal idata. Asynchronous
  * with respect to the host (stream-ordered). */
 tcfftResult tcfftExecC2C(tcfftHandle plan, const void* idata, void* odata);
+/* Same transform with HOST buffers (the reference's execute() works on host
+ * numpy data, executor.py:152): the batch is sliced and H2D copy, transform and
+ * D2H copy of successive slices are pipelined on three internal streams.
+ * hin/hout should be pinned (cudaHostAlloc / cudaHostRegister) for overlap;
+ * may alias.  Ordered after prior work on the plan's stream; completion is
+ * ordered before later work on it (synchronize the stream before reading hout). */
+tcfftResult tcfftExecC2CHost(tcfftHandle plan, const void* hin, void* hout);
 tcfftResult tcfftDestroy(tcfftHandle plan);
 
 const char* tcfftGetErrorString(tcfftResult r);

@@ -232,12 +232,41 @@ def execute(plan: Plan, data, out=None, stream=None):
     return o if out is not None else data
 
 
+def execute_host(plan: Plan, data, out=None, stream=None):
+    """Transform HOST data (torch CPU tensor, ideally pinned): the batch is
+    sliced and H2D / transform / D2H of successive slices are pipelined
+    (``tcfftExecC2CHost``).  In place by default; returns the host tensor.
+    Synchronises the stream before returning (the result is on the host)."""
+    import torch
+
+    if plan._handle is None:
+        raise ExecuteError("plan has been destroyed")
+    for t in (data,) + ((out,) if out is not None else ()):
+        if not isinstance(t, torch.Tensor) or t.is_cuda:
+            raise ExecuteError("execute_host needs CPU (host) tensors")
+        if t.dtype not in (torch.complex32, torch.float16) or not t.is_contiguous():
+            raise ExecuteError("host data must be contiguous complex32 / float16[..., 2]")
+    n = data.numel() // (1 if data.dtype == torch.complex32 else 2)
+    if n != plan.batch * plan.n_logical:
+        raise ExecuteError(f"data holds {n} complex elements, plan needs {plan.batch * plan.n_logical}")
+    o = data if out is None else out
+    L = _lib.load()
+    s = stream if stream is not None else torch.cuda.current_stream()
+    st = L.tcfftSetStream(plan._handle, ctypes.c_void_p(s.cuda_stream))
+    if st == _lib.TCFFT_SUCCESS:
+        st = L.tcfftExecC2CHost(plan._handle, ctypes.c_void_p(data.data_ptr()), ctypes.c_void_p(o.data_ptr()))
+    if st != _lib.TCFFT_SUCCESS:
+        raise ExecuteError(f"tcfftExecC2CHost failed: {_lib.error_string(st)}")
+    s.synchronize()
+    return o
+
+
 def flops_5nlogn(n_total: int, batch: int) -> float:
     """Headline flop count of the project metric: 5 N log2 N per transform."""
     return 5.0 * n_total * math.log2(n_total) * batch
 
 
 __all__ = [
-    "ExecuteError", "Plan", "PlanArgumentError", "UnsupportedSizeError", "execute", "flops_5nlogn",
+    "ExecuteError", "Plan", "PlanArgumentError", "UnsupportedSizeError", "execute", "execute_host", "flops_5nlogn",
     "plan_1d", "plan_2d", "schedule_radices",
 ]

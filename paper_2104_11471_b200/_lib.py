@@ -12,7 +12,7 @@ import json
 import os
 from pathlib import Path
 
-_LIB_PATH = Path(__file__).resolve().parent / "libtcfft_b200.so"
+_LIB_PATH = Path(os.environ.get("TCFFT_LIB") or (Path(__file__).resolve().parent / "libtcfft_b200.so"))
 _lib = None
 
 TCFFT_SUCCESS = 0
@@ -26,7 +26,7 @@ TCFFT_NO_DEVICE = 7
 
 # every symbol include/tcfft_b200.h declares
 EXPORTS = (
-    "tcfftPlan1D", "tcfftPlan2D", "tcfftSetStream", "tcfftGetWorkspaceSize", "tcfftExecC2C",
+    "tcfftPlan1D", "tcfftPlan2D", "tcfftSetStream", "tcfftGetWorkspaceSize", "tcfftExecC2C", "tcfftExecC2CHost",
     "tcfftDestroy", "tcfftGetErrorString", "tcfftGetVersion", "tcfftDescribePlan", "tcfftPlanTables",
 )
 
@@ -54,6 +54,8 @@ def load(build_if_missing: bool = True):
     L.tcfftSetStream.argtypes = [vp, vp]
     L.tcfftGetWorkspaceSize.argtypes = [vp, ctypes.POINTER(sz)]
     L.tcfftExecC2C.argtypes = [vp, vp, vp]
+    if hasattr(L, "tcfftExecC2CHost"):
+        L.tcfftExecC2CHost.argtypes = [vp, vp, vp]
     L.tcfftDestroy.argtypes = [vp]
     L.tcfftGetErrorString.argtypes = [ci]
     L.tcfftGetErrorString.restype = ctypes.c_char_p
@@ -62,7 +64,7 @@ def load(build_if_missing: bool = True):
     L.tcfftPlanTables.argtypes = [ci, ci, ci, ci, ci, vp, ctypes.POINTER(sz), vp, ctypes.POINTER(sz), vp,
                                   ctypes.POINTER(sz)]
     for name in EXPORTS:
-        if name not in ("tcfftGetErrorString",):
+        if name not in ("tcfftGetErrorString",) and hasattr(L, name):
             getattr(L, name).restype = ci
     _lib = L
     return L

@@ -34,14 +34,16 @@ def needs_build() -> bool:
     return any(p.stat().st_mtime > t for p in DEPS)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, out: Path | None = None) -> Path:
+    out = Path(out) if out else LIB
+    if out == LIB and not force and not needs_build():
         return LIB
     cmd = [
         nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
         "-shared", "-Xcompiler", "-fPIC", "-cudart", "static", "-I", str(ROOT / "include"),
         "-Xptxas", "-v" if verbose else "-O3",
-        "-o", str(LIB) + ".tmp", *map(str, SOURCES),
+        *[f"-D{d}" for d in os.environ.get("TCFFT_DEFINES", "").split(",") if d],
+        "-o", str(out) + ".tmp", *map(str, SOURCES),
     ]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
@@ -49,10 +51,12 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         raise RuntimeError("nvcc failed building libtcfft_b200.so")
     if verbose:
         sys.stderr.write(res.stderr)
-    os.replace(str(LIB) + ".tmp", LIB)
-    return LIB
+    os.replace(str(out) + ".tmp", out)
+    return out
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
-    print(LIB)
+    o = None
+    if "-o" in sys.argv:
+        o = sys.argv[sys.argv.index("-o") + 1]
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, out=o))

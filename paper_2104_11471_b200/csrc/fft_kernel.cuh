@@ -46,7 +46,7 @@ struct KParams {
   const RowInfo* rows_tab;
   const uint16_t* bblob;
   int32_t bbytes;
-  int32_t smem_a, smem_b, smem_bar, smem_tw4;
+  int32_t smem_a, a_stride, smem_b, smem_bar, smem_tw4;
   int64_t tw4_total;  // four-step pass 1: full transform length
   int32_t tw4_nk;     // number of final-stage k values (N1 / R_S)
   int32_t tw4_s;      // N1 / R_S
@@ -73,7 +73,17 @@ struct Cfg {
   __host__ __device__ static constexpr int T(int s) { return E / (128 * R(s)); }
   __host__ __device__ static constexpr int SBO(int s) { return 32 * R(s) + 16; }  // padded: consecutive 8-row groups hit distinct banks
   __host__ __device__ static constexpr int TILEB(int s) { return 16 * SBO(s); }
-  __host__ __device__ static constexpr int BOFF(int s) { return s == 0 ? 0 : BOFF(s - 1) + KP(s - 1) * NP(s - 1) * 2; }
+  // B matrices: stage 0 (interleaved K), then one planar-K matrix per distinct
+  // radix run (stages s >= 2 with R(s) == R(s-1) share the previous matrix)
+  __host__ __device__ static constexpr int BSZ(int s) { return KP(s) * NP(s) * 2; }
+#ifndef TCFFT_BDEDUPE
+  __host__ __device__ static constexpr bool BSHARE(int s) { return false; }
+#else
+  __host__ __device__ static constexpr bool BSHARE(int s) { return s >= 2 && R(s) == R(s - 1); }
+#endif
+  __host__ __device__ static constexpr int BOFF(int s) {
+    return s == 0 ? 0 : (BSHARE(s) ? BOFF(s - 1) : BOFF(s - 1) + (BSHARE(s - 1) ? 0 : BSZ(s - 1)));
+  }
   __host__ __device__ static constexpr int HSTEP(int s) { return (128 / R(s)) * SBO(s + 1); }
   __host__ __device__ static constexpr int IMOFF(int s) { return 16 * R(s + 1); }
   __host__ __device__ static constexpr int tmax(int a, int b) { return a > b ? a : b; }
@@ -123,6 +133,41 @@ DEVI void load_acc(uint32_t taddr, float* x) {
   }
   tmem_wait_ld();
 }
+
+// Load K consecutive 32-bit TMEM columns of this thread's lane (no wait).
+template <int K>
+DEVI void tmem_ld_words(uint32_t taddr, uint32_t* r) {
+  if constexpr (K >= 8) {
+    tmem_ld8(taddr, r);
+    tmem_ld_words<K - 8>(taddr + 8, r + 8);
+  } else if constexpr (K >= 4) {
+    tmem_ld4(taddr, r);
+    tmem_ld_words<K - 4>(taddr + 4, r + 4);
+  } else if constexpr (K >= 2) {
+    tmem_ld2(taddr, r);
+    tmem_ld_words<K - 2>(taddr + 2, r + 2);
+  } else if constexpr (K == 1) {
+    tmem_ld1(taddr, r);
+  }
+}
+
+// Per-thread row records (host-built RowInfo fields) kept in spare TMEM
+// columns instead of registers: [stage-1 gather bases | per writer stage and
+// tile: addr, w (, c) | per final tile: addr (, k, c, w)].
+template <class C, bool TW4>
+struct Rec {
+  __host__ __device__ static constexpr int WS(int s) { return s == 0 ? 3 : 5; }
+  static constexpr int FW = TW4 ? 6 : 1;
+  __host__ __device__ static constexpr int OFF_W(int s) { return s == 0 ? C::T(0) : OFF_W(s - 1) + C::T(s - 1) * WS(s - 1); }
+  static constexpr int OFF_F = OFF_W(C::S - 1);
+  static constexpr int N = OFF_F + C::T(C::S - 1) * FW;
+  static constexpr int COL = C::DCOLS + C::ACOLS;
+#ifndef TCFFT_TMEMREC
+  static constexpr bool IN_TMEM = false;
+#else
+  static constexpr bool IN_TMEM = COL + N <= (int)C::COLS;
+#endif
+};
 
 DEVI float2 neg2(float2 a) { return make_float2(-a.x, -a.y); }  // folded into FFMA2 operand negation
 
@@ -346,15 +391,19 @@ __global__ void __launch_bounds__(128, MINB)
   constexpr int S = C::S;
   constexpr int TM = C::TMAX;
 
+#ifndef TCFFT_NO_ALIGN_SLACK
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+#else
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw;
+#endif
   uint8_t* s_in = smem;
-  uint8_t* s_a = smem + p.smem_a;
   uint8_t* s_b = smem + p.smem_b;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.smem_bar);
   uint32_t* s_tmem = reinterpret_cast<uint32_t*>(bars + 2);
   const int tid = threadIdx.x, warp = tid >> 5;
-  const uint32_t s_in_u = smem_u32(s_in), s_a_u = smem_u32(s_a), s_b_u = smem_u32(s_b);
+  const uint32_t s_in_u = smem_u32(s_in), s_b_u = smem_u32(s_b);
 
   // constants: B matrices, once per CTA
   for (int i = tid; i < p.bbytes / 16; i += 128)
@@ -371,6 +420,8 @@ __global__ void __launch_bounds__(128, MINB)
   // per-thread row records (host-built, see plan.cpp)
   auto rec = [&](int s, int t) -> const RowInfo& { return p.rows_tab[((size_t)s * p.tiles_max + t) * 128 + tid]; };
   // stage-0 writers have c = 1; the final stage needs only its output address
+  using RC = Rec<C, TW4>;
+  constexpr bool RT = RC::IN_TMEM;
   int gb[C::T(0)];
   int fk[TW4 ? C::T(S - 1) : 1];
   int waddr[S][TM];
@@ -398,14 +449,55 @@ __global__ void __launch_bounds__(128, MINB)
   const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
   const uint32_t tD = tbase;
   const uint32_t tA = tbase + (uint32_t)C::DCOLS;
+  const uint32_t tR = tbase + (uint32_t)RC::COL + lane_off;  // this lane's row records
+  if constexpr (RT) {
+    uint32_t w[RC::N];
+#pragma unroll
+    for (int t = 0; t < C::T(0); ++t) w[t] = (uint32_t)gb[t];
+#pragma unroll
+    for (int s = 0; s + 1 < S; ++s)
+#pragma unroll
+      for (int t = 0; t < C::T(s); ++t) {
+        uint32_t* q = w + RC::OFF_W(s) + t * RC::WS(s);
+        q[0] = (uint32_t)waddr[s][t];
+        q[1] = __float_as_uint(ww[s][t].x);
+        q[2] = __float_as_uint(ww[s][t].y);
+        if (s >= 1) {
+          q[3] = __float_as_uint(wc[s][t].x);
+          q[4] = __float_as_uint(wc[s][t].y);
+        }
+      }
+#pragma unroll
+    for (int t = 0; t < C::T(S - 1); ++t) {
+      uint32_t* q = w + RC::OFF_F + t * RC::FW;
+      q[0] = (uint32_t)waddr[S - 1][t];
+      if constexpr (TW4) {
+        q[1] = (uint32_t)fk[t];
+        q[2] = __float_as_uint(wc[S - 1][t].x);
+        q[3] = __float_as_uint(wc[S - 1][t].y);
+        q[4] = __float_as_uint(ww[S - 1][t].x);
+        q[5] = __float_as_uint(ww[S - 1][t].y);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < RC::N; ++i) tmem_st1(tR + i, w + i);
+    tmem_wait_st();
+  }
 
   float2* s_tw4 = reinterpret_cast<float2*>(smem + p.smem_tw4);
 
   int64_t chunk = blockIdx.x;
   if (tid == 0 && chunk < p.chunks) issue_load(&tm_in, p.in, p.T, chunk, s_in, &bars[0]);
-  uint32_t ld_phase = 0, mma_phase = 0;
+  uint32_t ld_phase = 0, mma_phase = 0, abuf = 0;
 
-  for (; chunk < p.chunks; chunk += gridDim.x) {
+  for (; chunk < p.chunks; chunk += gridDim.x, abuf ^= 1) {
+    // this chunk's A operand / output staging buffer (ping-pong)
+#ifndef TCFFT_PINGPONG
+    uint8_t* const s_a = smem + p.smem_a;
+#else
+    uint8_t* const s_a = smem + p.smem_a + abuf * p.a_stride;
+#endif
+    const uint32_t s_a_u = smem_u32(s_a);
     if constexpr (TW4) {
       // four-step twiddle, strip-base part: A[k] = W_Ntot^{base k}, r = W_Ntot^{base s}
       const int64_t base = (chunk % p.in.spi) * (int64_t)p.in.C;
@@ -419,9 +511,17 @@ __global__ void __launch_bounds__(128, MINB)
     mbar_wait(&bars[0], ld_phase);
     ld_phase ^= 1;
     // ---------------- stage 1: gather -> TMEM A
+    int g1[C::T(0)];
+    if constexpr (RT) {
+      tmem_ld_words<C::T(0)>(tR, reinterpret_cast<uint32_t*>(g1));
+      tmem_wait_ld();
+    } else {
+#pragma unroll
+      for (int t = 0; t < C::T(0); ++t) g1[t] = gb[t];
+    }
 #pragma unroll
     for (int t = 0; t < C::T(0); ++t)
-      gather_to_tmem<C>(s_in_u, gb[t], p.gstride, (uint32_t)p.swz_in, tA + lane_off + t * (C::KP(0) / 2));
+      gather_to_tmem<C>(s_in_u, g1[t], p.gstride, (uint32_t)p.swz_in, tA + lane_off + t * (C::KP(0) / 2));
     tmem_wait_st();
     tc_fence_before();
     __syncthreads();
@@ -429,7 +529,9 @@ __global__ void __launch_bounds__(128, MINB)
       tc_fence_after();
       int64_t nxt = chunk + gridDim.x;
       if (nxt < p.chunks) issue_load(&tm_in, p.in, p.T, nxt, s_in, &bars[0]);  // staging buffer is free again
-      bulk_wait_read0();  // previous chunk's output store no longer reads s_a
+      // the store that last read this s_a buffer is done (two iterations ago
+      // with ping-pong buffers, the previous one otherwise)
+      if (p.a_stride) bulk_wait_read1(); else bulk_wait_read0();
       issue_stage_mma<C, 0>(s_a_u, s_b_u, tD, tA);
       mma_commit(&bars[1]);
     }
@@ -440,10 +542,27 @@ __global__ void __launch_bounds__(128, MINB)
     // ---------------- stages 2..S
     auto writer = [&](auto sc) {
       constexpr int s = decltype(sc)::value;
+      uint32_t rw[C::T(s) * RC::WS(s)];
+      if constexpr (RT) {
+        tmem_ld_words<C::T(s) * RC::WS(s)>(tR + RC::OFF_W(s), rw);
+        tmem_wait_ld();
+      }
 #pragma unroll
-      for (int t = 0; t < C::T(s); ++t)
-        writer_epilogue<C, s>(tD + lane_off + t * C::NP(s), s_a_u + waddr[s][t],
-                              s == 0 ? make_float2(1.f, 0.f) : wc[s][t], ww[s][t]);
+      for (int t = 0; t < C::T(s); ++t) {
+        int ad;
+        float2 cc = make_float2(1.f, 0.f), wv;
+        if constexpr (RT) {
+          const uint32_t* q = rw + t * RC::WS(s);
+          ad = (int)q[0];
+          wv = make_float2(__uint_as_float(q[1]), __uint_as_float(q[2]));
+          if constexpr (s >= 1) cc = make_float2(__uint_as_float(q[3]), __uint_as_float(q[4]));
+        } else {
+          ad = waddr[s][t];
+          wv = ww[s][t];
+          if constexpr (s >= 1) cc = wc[s][t];
+        }
+        writer_epilogue<C, s>(tD + lane_off + t * C::NP(s), s_a_u + ad, cc, wv);
+      }
       fence_proxy_async_smem();
       tc_fence_before();
       __syncthreads();
@@ -459,16 +578,33 @@ __global__ void __launch_bounds__(128, MINB)
     if constexpr (S >= 2) writer(std::integral_constant<int, 0>{});
     if constexpr (S >= 3) writer(std::integral_constant<int, 1>{});
     // ---------------- final epilogue -> output staging (reuses s_a)
+    uint32_t rf[C::T(S - 1) * RC::FW];
+    if constexpr (RT) {
+      tmem_ld_words<C::T(S - 1) * RC::FW>(tR + RC::OFF_F, rf);
+      tmem_wait_ld();
+    }
 #pragma unroll
     for (int t = 0; t < C::T(S - 1); ++t) {
       float2 c4 = make_float2(1.f, 0.f), w4 = make_float2(1.f, 0.f);
+      int ad = RT ? (int)rf[t * RC::FW] : waddr[S - 1][t];
       if constexpr (TW4) {
-        const float2 a = s_tw4[fk[t]], r = s_tw4[p.tw4_nk], hc = wc[S - 1][t], hw = ww[S - 1][t];
+        int kk;
+        float2 hc, hw;
+        if constexpr (RT) {
+          const uint32_t* q = rf + t * RC::FW;
+          kk = (int)q[1];
+          hc = make_float2(__uint_as_float(q[2]), __uint_as_float(q[3]));
+          hw = make_float2(__uint_as_float(q[4]), __uint_as_float(q[5]));
+        } else {
+          kk = fk[t];
+          hc = wc[S - 1][t];
+          hw = ww[S - 1][t];
+        }
+        const float2 a = s_tw4[kk], r = s_tw4[p.tw4_nk];
         c4 = make_float2(a.x * hc.x - a.y * hc.y, a.x * hc.y + a.y * hc.x);
         w4 = make_float2(r.x * hw.x - r.y * hw.y, r.x * hw.y + r.y * hw.x);
       }
-      final_epilogue<C, TW4>(tD + lane_off + t * C::NP(S - 1), s_a_u, waddr[S - 1][t], p.ostride,
-                             (uint32_t)p.swz_out, c4, w4);
+      final_epilogue<C, TW4>(tD + lane_off + t * C::NP(S - 1), s_a_u, ad, p.ostride, (uint32_t)p.swz_out, c4, w4);
     }
     fence_proxy_async_smem();
     tc_fence_before();

@@ -369,8 +369,16 @@ bool build_pass(PassPlan& p, int kind, int N, int64_t count, int64_t images, int
   for (int s = 0; s < S; ++s) {
     StageInfo& st = p.st[s];
     const int R = st.R, KP = st.KP, NP = st.NP;
-    st.b_off = (int)(p.bblob.size() * 2);
     st.b_bytes = KP * NP * 2;
+#ifdef TCFFT_BDEDUPE
+    if (s >= 2 && p.st[s - 1].R == R) {  // identical planar-K matrix: share it
+#else
+    if (false) {
+#endif
+      st.b_off = p.st[s - 1].b_off;
+      continue;
+    }
+    st.b_off = (int)(p.bblob.size() * 2);
     std::vector<uint16_t> blob(KP * NP, 0);
     for (int k = 0; k < KP; ++k)
       for (int n = 0; n < NP; ++n) {
@@ -404,6 +412,13 @@ bool build_pass(PassPlan& p, int kind, int N, int64_t count, int64_t images, int
 
   // ---- shared memory / TMEM budget ---------------------------------------
   const int stage_bytes = row_in ? T * PW * 4 : E * 4;
+  {
+    int acols = p.st[0].tiles * (p.st[0].KP / 2), dcols = 0;
+    for (int s2 = 0; s2 < S; ++s2) dcols = std::max(dcols, p.st[s2].tiles * p.st[s2].NP);
+    int need = acols + dcols, tc = 32;
+    while (tc < need) tc <<= 1;
+    p.tmem_cols_needed = tc;
+  }
   const int tw4_bytes = tw4_total ? ((N / rad[S - 1]) * 8 + 16 + 127) & ~127 : 0;
   int a_bytes = stage_bytes;
   for (int s = 1; s < S; ++s) a_bytes = std::max(a_bytes, p.st[s].tiles * p.st[s].tile_bytes);
@@ -411,12 +426,31 @@ bool build_pass(PassPlan& p, int kind, int N, int64_t count, int64_t images, int
   p.a_bytes = a_bytes;
   p.smem_in = 0;
   p.smem_a = (stage_bytes + 1023) & ~1023;
-  p.smem_b = p.smem_a + a_bytes;
+  // two A / output-staging buffers: chunk i's epilogues never wait for the TMA
+  // store of chunk i-1 to finish reading its staging tile
+  // (only when that still leaves room for the TMEM-limited number of CTAs/SM)
+  {
+    const int fixed = p.smem_a + a_bytes + (((int)p.bblob.size() * 2 + 127) & ~127) + tw4_bytes + 64 + 1024;
+    const int tmem_ctas = std::max(1, 512 / std::max(32, p.tmem_cols_needed));
+#ifdef TCFFT_PINGPONG
+    p.a_bufs = (fixed + a_bytes) * std::min(tmem_ctas, 4) <= 233472 ? 2 : 1;
+#else
+    p.a_bufs = 1;
+    (void)fixed;
+    (void)tmem_ctas;
+#endif
+    if (const char* e = std::getenv("TCFFT_ABUFS")) p.a_bufs = std::max(1, std::min(2, std::atoi(e)));
+  }
+  p.smem_b = p.smem_a + p.a_bufs * a_bytes;
   int bsz = ((int)p.bblob.size() * 2 + 127) & ~127;
   p.smem_t = p.smem_b + bsz;
   p.smem_tw4 = p.smem_t;
   p.smem_bar = p.smem_tw4 + tw4_bytes;
-  p.smem_bytes = p.smem_bar + 64 /*mbarriers + TMEM address*/ + 1024 /*alignment slack*/;
+#ifndef TCFFT_NO_ALIGN_SLACK
+  p.smem_bytes = p.smem_bar + 64 + 1024;
+#else
+  p.smem_bytes = p.smem_bar + 64 /*mbarriers + TMEM address*/;
+#endif
   int acols = p.st[0].tiles * (p.st[0].KP / 2);
   int dcols = 0;
   for (int s = 0; s < S; ++s) dcols = std::max(dcols, p.st[s].tiles * p.st[s].NP);
@@ -429,7 +463,7 @@ bool build_pass(PassPlan& p, int kind, int N, int64_t count, int64_t images, int
   p.tmem_cols = tcols;
   p.tmem_a_cols = dcols;  // A region starts after D
   int by_tmem = 512 / tcols;
-  int by_smem = (227 * 1024) / p.smem_bytes;
+  int by_smem = 233472 / (p.smem_bytes + 1024);  // 228 KB per SM incl. 1 KB driver reserve per CTA
   p.ctas_per_sm = std::max(1, std::min(by_tmem, std::min(by_smem, 4)));
   return true;
 }

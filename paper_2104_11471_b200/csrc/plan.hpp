@@ -97,6 +97,8 @@ struct PassPlan {
   int32_t tmem_cols; // allocation (power of two >= 32)
   int32_t tmem_a_cols;
   int32_t ctas_per_sm;
+  int32_t a_bufs;            // 1 or 2 A / output-staging buffers
+  int32_t tmem_cols_needed;
   std::vector<RowInfo> rows_tab;   // [S][tiles_max][128]
   int32_t tiles_max;
   std::vector<uint16_t> bblob;     // fp16 B matrices, UMMA K-major core-matrix order

@@ -90,10 +90,13 @@ struct DevPass {
 
 }  // namespace
 
+struct HostPipe;
+
 struct tcfftPlanImpl {
   tcfft::Plan plan;
   std::vector<DevPass> dev;
   void* ws = nullptr;
+  HostPipe* pipe = nullptr;  // lazily built by tcfftExecC2CHost
   cudaStream_t stream = nullptr;
   int device = 0;
   int magic = 0x7cff7;
@@ -223,6 +226,7 @@ tcfftResult create(tcfftHandle* out, int dims, int nx, int ny, int batch) {
     k.bblob = reinterpret_cast<const uint16_t*>(base + rb_al);
     k.bbytes = (int)(p.bblob.size() * 2);  // multiple of 512
     k.smem_a = p.smem_a;
+    k.a_stride = p.a_bufs == 2 ? p.a_bytes : 0;
     k.smem_b = p.smem_b;
     k.smem_bar = p.smem_bar;
     k.smem_tw4 = p.smem_tw4;
@@ -295,10 +299,129 @@ tcfftResult tcfftExecC2C(tcfftHandle plan, const void* idata, void* odata) {
   return TCFFT_SUCCESS;
 }
 
+// ---------------------------------------------------------------------------
+// Host-buffer execution: the batch is cut into slices of whole transforms;
+// slice i's H2D copy, transform and D2H copy run on three streams, ring of
+// three device slice buffers, so both PCIe directions and the tensor-core
+// kernels overlap.  Pinned host memory is needed for real overlap.
+struct HostPipe {
+  int64_t slice_batch = 0, slices = 0, tail = 0;
+  tcfftHandle full = nullptr, last = nullptr;  // sub-plans (slice batch, tail batch)
+  void* dbuf[3] = {nullptr, nullptr, nullptr};
+  cudaStream_t s[3] = {nullptr, nullptr, nullptr};  // h2d, compute, d2h
+  cudaEvent_t ev_in[3], ev_done[3], ev_free[3], ev_start, ev_end;
+  bool ok = false;
+};
+
+static void destroy_pipe(HostPipe* hp) {
+  if (!hp) return;
+  if (hp->full) tcfftDestroy(hp->full);
+  if (hp->last) tcfftDestroy(hp->last);
+  for (int i = 0; i < 3; ++i) {
+    if (hp->dbuf[i]) cudaFree(hp->dbuf[i]);
+    if (hp->s[i]) cudaStreamDestroy(hp->s[i]);
+    if (hp->ok) {
+      cudaEventDestroy(hp->ev_in[i]);
+      cudaEventDestroy(hp->ev_done[i]);
+      cudaEventDestroy(hp->ev_free[i]);
+    }
+  }
+  if (hp->ok) {
+    cudaEventDestroy(hp->ev_start);
+    cudaEventDestroy(hp->ev_end);
+  }
+  delete hp;
+}
+
+static tcfftResult build_pipe(tcfftHandle plan) {
+  const tcfft::Plan& P = plan->plan;
+  const int64_t n = (int64_t)P.nx * (P.dims == 2 ? P.ny : 1);
+  const int64_t bytes_per = n * 4;
+  auto* hp = new (std::nothrow) HostPipe();
+  if (!hp) return TCFFT_ALLOC_FAILED;
+  const int64_t target = 32ll << 20;  // ~32 MiB slices
+  hp->slice_batch = std::max<int64_t>(1, std::min<int64_t>(P.batch, target / bytes_per));
+  hp->slices = (P.batch + hp->slice_batch - 1) / hp->slice_batch;
+  hp->tail = P.batch - (hp->slices - 1) * hp->slice_batch;
+  tcfftResult st = P.dims == 1 ? tcfftPlan1D(&hp->full, P.nx, (int)hp->slice_batch)
+                               : tcfftPlan2D(&hp->full, P.nx, P.ny, (int)hp->slice_batch);
+  if (st == TCFFT_SUCCESS && hp->tail != hp->slice_batch)
+    st = P.dims == 1 ? tcfftPlan1D(&hp->last, P.nx, (int)hp->tail) : tcfftPlan2D(&hp->last, P.nx, P.ny, (int)hp->tail);
+  for (int i = 0; i < 3 && st == TCFFT_SUCCESS; ++i) {
+    if (cudaMalloc(&hp->dbuf[i], (size_t)(hp->slice_batch * bytes_per)) != cudaSuccess) st = TCFFT_ALLOC_FAILED;
+    if (cudaStreamCreateWithFlags(&hp->s[i], cudaStreamNonBlocking) != cudaSuccess) st = TCFFT_EXEC_FAILED;
+  }
+  if (st == TCFFT_SUCCESS) {
+    for (int i = 0; i < 3; ++i) {
+      cudaEventCreateWithFlags(&hp->ev_in[i], cudaEventDisableTiming);
+      cudaEventCreateWithFlags(&hp->ev_done[i], cudaEventDisableTiming);
+      cudaEventCreateWithFlags(&hp->ev_free[i], cudaEventDisableTiming);
+    }
+    cudaEventCreateWithFlags(&hp->ev_start, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&hp->ev_end, cudaEventDisableTiming);
+    hp->ok = true;
+  }
+  if (st != TCFFT_SUCCESS) {
+    cudaGetLastError();
+    destroy_pipe(hp);
+    return st;
+  }
+  plan->pipe = hp;
+  return TCFFT_SUCCESS;
+}
+
+extern "C" tcfftResult tcfftExecC2CHost(tcfftHandle plan, const void* hin, void* hout) {
+  if (!valid(plan)) return TCFFT_INVALID_PLAN;
+  if (!hin || !hout) return TCFFT_INVALID_VALUE;
+  if (!plan->pipe) {
+    tcfftResult st = build_pipe(plan);
+    if (st != TCFFT_SUCCESS) return st;
+  }
+  HostPipe* hp = plan->pipe;
+  const tcfft::Plan& P = plan->plan;
+  const int64_t bytes_per = (int64_t)P.nx * (P.dims == 2 ? P.ny : 1) * 4;
+  const char* src = static_cast<const char*>(hin);
+  char* dst = static_cast<char*>(hout);
+  if (hp->slices == 1) {  // small problem: one slice, the plan's own stream, no cross-stream events
+    const size_t bytes = (size_t)(P.batch * bytes_per);
+    cudaMemcpyAsync(hp->dbuf[0], src, bytes, cudaMemcpyHostToDevice, plan->stream);
+    tcfftSetStream(hp->full, plan->stream);
+    tcfftResult st = tcfftExecC2C(hp->full, hp->dbuf[0], hp->dbuf[0]);
+    if (st != TCFFT_SUCCESS) return st;
+    cudaMemcpyAsync(dst, hp->dbuf[0], bytes, cudaMemcpyDeviceToHost, plan->stream);
+    return cudaGetLastError() == cudaSuccess ? TCFFT_SUCCESS : TCFFT_EXEC_FAILED;
+  }
+  // order after earlier work on the plan's stream
+  cudaEventRecord(hp->ev_start, plan->stream);
+  cudaStreamWaitEvent(hp->s[0], hp->ev_start, 0);
+  for (int64_t i = 0; i < hp->slices; ++i) {
+    const int b = (int)(i % 3);
+    const int64_t nb = (i + 1 == hp->slices) ? hp->tail : hp->slice_batch;
+    const size_t bytes = (size_t)(nb * bytes_per);
+    const size_t off = (size_t)(i * hp->slice_batch * bytes_per);
+    if (i >= 3) cudaStreamWaitEvent(hp->s[0], hp->ev_free[b], 0);  // slice i-3 drained
+    cudaMemcpyAsync(hp->dbuf[b], src + off, bytes, cudaMemcpyHostToDevice, hp->s[0]);
+    cudaEventRecord(hp->ev_in[b], hp->s[0]);
+    cudaStreamWaitEvent(hp->s[1], hp->ev_in[b], 0);
+    tcfftHandle sub = (nb == hp->slice_batch) ? hp->full : hp->last;
+    tcfftSetStream(sub, hp->s[1]);
+    tcfftResult st = tcfftExecC2C(sub, hp->dbuf[b], hp->dbuf[b]);
+    if (st != TCFFT_SUCCESS) return st;
+    cudaEventRecord(hp->ev_done[b], hp->s[1]);
+    cudaStreamWaitEvent(hp->s[2], hp->ev_done[b], 0);
+    cudaMemcpyAsync(dst + off, hp->dbuf[b], bytes, cudaMemcpyDeviceToHost, hp->s[2]);
+    cudaEventRecord(hp->ev_free[b], hp->s[2]);
+  }
+  cudaEventRecord(hp->ev_end, hp->s[2]);
+  cudaStreamWaitEvent(plan->stream, hp->ev_end, 0);
+  return cudaGetLastError() == cudaSuccess ? TCFFT_SUCCESS : TCFFT_EXEC_FAILED;
+}
+
 tcfftResult tcfftDestroy(tcfftHandle plan) {
   if (!valid(plan)) return TCFFT_INVALID_PLAN;
   for (auto& q : plan->dev) cudaFree(q.tables);
   if (plan->ws) cudaFree(plan->ws);
+  destroy_pipe(plan->pipe);
   plan->magic = 0;
   delete plan;
   return TCFFT_SUCCESS;
@@ -347,7 +470,7 @@ tcfftResult tcfftDescribePlan(int dims, int nx, int ny, int batch, char* json, s
            ", \"smem_bytes\": " + std::to_string(p.smem_bytes) + ", \"smem_a\": " + std::to_string(p.smem_a) +
            ", \"a_bytes\": " + std::to_string(p.a_bytes) + ", \"tmem_cols\": " + std::to_string(p.tmem_cols) +
            ", \"tmem_a_col\": " + std::to_string(p.tmem_a_cols) +
-           ", \"ctas_per_sm\": " + std::to_string(p.ctas_per_sm) + ", \"tiles_max\": " +
+           ", \"ctas_per_sm\": " + std::to_string(p.ctas_per_sm) + ", \"a_bufs\": " + std::to_string(p.a_bufs) + ", \"tiles_max\": " +
            std::to_string(p.tiles_max) + ", \"stages\": [";
       for (int sidx = 0; sidx < p.S; ++sidx) {
         const auto& t = p.st[sidx];

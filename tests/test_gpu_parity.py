@@ -183,3 +183,21 @@ def test_config_c4_2d_512x512_batch1024():
 
 def test_config_c3_n2pow22_batch64():
     _config_check(1 << 22, None, 64, 1)
+
+
+@pytest.mark.parametrize("nx,ny,batch", [(4096, None, 2048), (256, None, 3000), (1 << 16, None, 3), (512, 512, 5)])
+def test_execute_host_matches_device_path(nx, ny, batch):
+    """tcfftExecC2CHost (sliced, pipelined host-buffer path) == device path."""
+    tc = _tc()
+    total = nx * (ny or 1)
+    g = torch.Generator(device="cuda").manual_seed(77)
+    x = (torch.rand((batch, total, 2), device="cuda", generator=g) * 2 - 1).half()
+    plan = tc.plan_1d(nx, batch) if ny is None else tc.plan_2d(nx, ny, batch)
+    y = torch.empty_like(x)
+    tc.execute(plan, x, out=y)
+    h = x.cpu().pin_memory()
+    ho = torch.empty_like(h).pin_memory()
+    tc.execute_host(plan, h, out=ho)
+    assert torch.equal(ho.view(torch.int16), y.cpu().view(torch.int16))
+    tc.execute_host(plan, h)  # in place on the host
+    assert torch.equal(h.view(torch.int16), y.cpu().view(torch.int16))
