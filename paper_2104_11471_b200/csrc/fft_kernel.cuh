@@ -50,6 +50,7 @@ struct KParams {
   int64_t tw4_total;  // four-step pass 1: full transform length
   int32_t tw4_nk;     // number of final-stage k values (N1 / R_S)
   int32_t tw4_s;      // N1 / R_S
+  int32_t gather_ahead;  // gather chunk i+1 while chunk i's last MMAs run
 };
 
 namespace dev {
@@ -411,7 +412,7 @@ __global__ void __launch_bounds__(128, MINB)
   if (warp == 0) tmem_alloc<C::COLS>(s_tmem);
   if (tid == 0) {
     mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
+    mbar_init(&bars[1], 2);  // tcgen05.commit + thread 0's arrive
     fence_mbar_init();
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_in) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_out) : "memory");
@@ -486,32 +487,16 @@ __global__ void __launch_bounds__(128, MINB)
 
   float2* s_tw4 = reinterpret_cast<float2*>(smem + p.smem_tw4);
 
-  int64_t chunk = blockIdx.x;
-  if (tid == 0 && chunk < p.chunks) issue_load(&tm_in, p.in, p.T, chunk, s_in, &bars[0]);
-  uint32_t ld_phase = 0, mma_phase = 0, abuf = 0;
-
-  for (; chunk < p.chunks; chunk += gridDim.x, abuf ^= 1) {
-    // this chunk's A operand / output staging buffer (ping-pong)
-#ifndef TCFFT_PINGPONG
-    uint8_t* const s_a = smem + p.smem_a;
-#else
-    uint8_t* const s_a = smem + p.smem_a + abuf * p.a_stride;
-#endif
-    const uint32_t s_a_u = smem_u32(s_a);
-    if constexpr (TW4) {
-      // four-step twiddle, strip-base part: A[k] = W_Ntot^{base k}, r = W_Ntot^{base s}
-      const int64_t base = (chunk % p.in.spi) * (int64_t)p.in.C;
-      for (int kk = tid; kk <= p.tw4_nk; kk += 128) {
-        const int64_t e = (base * (kk < p.tw4_nk ? kk : p.tw4_s)) % p.tw4_total;
-        float sn, cs;
-        sincospif(-2.0f * (float)e / (float)p.tw4_total, &sn, &cs);
-        s_tw4[kk] = make_float2(cs, sn);
-      }
-    }
-    mbar_wait(&bars[0], ld_phase);
-    ld_phase ^= 1;
-    // ---------------- stage 1: gather -> TMEM A
-    int g1[C::T(0)];
+  // ---------------------------------------------------------------------
+  // Software-pipelined chunk loop.  The MMA barrier (bars[1]) completes on two
+  // arrivals: the tcgen05.commit of the stage's MMAs and a plain arrive by
+  // thread 0 (issued after any wait thread 0 owes the other warps, e.g. the
+  // previous output store releasing s_a), so thread 0 never delays MMA issue.
+  // While the last stage's MMAs of chunk i run, all threads already gather
+  // chunk i+1 into the (idle) stage-1 TMEM A region.
+  uint32_t ld_phase = 0, mma_phase = 0;
+  const int64_t chunk0 = blockIdx.x;
+  auto rec_g1 = [&](int* g1) {
     if constexpr (RT) {
       tmem_ld_words<C::T(0)>(tR, reinterpret_cast<uint32_t*>(g1));
       tmem_wait_ld();
@@ -519,30 +504,62 @@ __global__ void __launch_bounds__(128, MINB)
 #pragma unroll
       for (int t = 0; t < C::T(0); ++t) g1[t] = gb[t];
     }
+  };
+  auto tw4_table = [&](int64_t ch) {
+    if constexpr (TW4) {
+      // four-step twiddle, strip-base part: A[k] = W_Ntot^{base k}, r = W_Ntot^{base s}
+      const int64_t base = (ch % p.in.spi) * (int64_t)p.in.C;
+      for (int kk = tid; kk <= p.tw4_nk; kk += 128) {
+        const int64_t e = (base * (kk < p.tw4_nk ? kk : p.tw4_s)) % p.tw4_total;
+        float sn, cs;
+        sincospif(-2.0f * (float)e / (float)p.tw4_total, &sn, &cs);
+        s_tw4[kk] = make_float2(cs, sn);
+      }
+    }
+  };
+  // stage-1 gather of `ch` (its TMA load must have been issued)
+  auto gather = [&]() {
+    mbar_wait(&bars[0], ld_phase);
+    ld_phase ^= 1;
+    int g1[C::T(0)];
+    rec_g1(g1);
 #pragma unroll
     for (int t = 0; t < C::T(0); ++t)
       gather_to_tmem<C>(s_in_u, g1[t], p.gstride, (uint32_t)p.swz_in, tA + lane_off + t * (C::KP(0) / 2));
     tmem_wait_st();
+  };
+  auto wait_mma = [&]() {
+    mbar_wait(&bars[1], mma_phase);
+    mma_phase ^= 1;
+    tc_fence_after();
+  };
+  uint8_t* const s_a = smem + p.smem_a;
+  const uint32_t s_a_u = smem_u32(s_a);
+
+  if (chunk0 < p.chunks) {
+    if (tid == 0) issue_load(&tm_in, p.in, p.T, chunk0, s_in, &bars[0]);
+    gather();
     tc_fence_before();
     __syncthreads();
     if (tid == 0) {
       tc_fence_after();
-      int64_t nxt = chunk + gridDim.x;
-      if (nxt < p.chunks) issue_load(&tm_in, p.in, p.T, nxt, s_in, &bars[0]);  // staging buffer is free again
-      // the store that last read this s_a buffer is done (two iterations ago
-      // with ping-pong buffers, the previous one otherwise)
-      if (p.a_stride) bulk_wait_read1(); else bulk_wait_read0();
+      if (chunk0 + gridDim.x < p.chunks) issue_load(&tm_in, p.in, p.T, chunk0 + gridDim.x, s_in, &bars[0]);
       issue_stage_mma<C, 0>(s_a_u, s_b_u, tD, tA);
       mma_commit(&bars[1]);
+      mbar_arrive(&bars[1]);
     }
-    mbar_wait(&bars[1], mma_phase);
-    mma_phase ^= 1;
-    tc_fence_after();
+  }
 
-    // ---------------- stages 2..S
+  for (int64_t chunk = chunk0; chunk < p.chunks; chunk += gridDim.x) {
+    const int64_t next = chunk + gridDim.x;
+    const bool has_next = next < p.chunks;
+    tw4_table(chunk);
+
+    // ---------------- writer stages: wait MMA s, epilogue s, issue MMA s+1
     auto writer = [&](auto sc) {
       constexpr int s = decltype(sc)::value;
-      uint32_t rw[C::T(s) * RC::WS(s)];
+      wait_mma();
+      [[maybe_unused]] uint32_t rw[C::T(s) * RC::WS(s)];
       if constexpr (RT) {
         tmem_ld_words<C::T(s) * RC::WS(s)>(tR + RC::OFF_W(s), rw);
         tmem_wait_ld();
@@ -570,13 +587,22 @@ __global__ void __launch_bounds__(128, MINB)
         tc_fence_after();
         issue_stage_mma<C, s + 1>(s_a_u, s_b_u, tD, tA);
         mma_commit(&bars[1]);
+        mbar_arrive(&bars[1]);
       }
-      mbar_wait(&bars[1], mma_phase);
-      mma_phase ^= 1;
-      tc_fence_after();
     };
     if constexpr (S >= 2) writer(std::integral_constant<int, 0>{});
     if constexpr (S >= 3) writer(std::integral_constant<int, 1>{});
+
+    // ---------------- overlap: gather the next chunk while the last MMAs run
+    // (single-stage plans: the last MMA reads the TMEM A region, wait first)
+    if (S >= 2 && p.gather_ahead) {
+      if (has_next) gather();
+      wait_mma();
+    } else {
+      wait_mma();
+      if (has_next) gather();
+    }
+
     // ---------------- final epilogue -> output staging (reuses s_a)
     uint32_t rf[C::T(S - 1) * RC::FW];
     if constexpr (RT) {
@@ -609,7 +635,20 @@ __global__ void __launch_bounds__(128, MINB)
     fence_proxy_async_smem();
     tc_fence_before();
     __syncthreads();
-    if (tid == 0) issue_store(&tm_out, p.out, p.T, chunk, s_a);
+    if (tid == 0) {
+      tc_fence_after();
+      issue_store(&tm_out, p.out, p.T, chunk, s_a);
+      if (has_next) {
+        // next chunk: its staging buffer is free (gathered above): prefetch the
+        // one after, start its stage-1 MMAs, then release the epilogue warps
+        // once the store just issued has finished reading s_a
+        if (next + gridDim.x < p.chunks) issue_load(&tm_in, p.in, p.T, next + gridDim.x, s_in, &bars[0]);
+        issue_stage_mma<C, 0>(s_a_u, s_b_u, tD, tA);
+        mma_commit(&bars[1]);
+        bulk_wait_read0();
+        mbar_arrive(&bars[1]);
+      }
+    }
   }
   if (tid == 0) bulk_wait0();
   tc_fence_before();

@@ -5,6 +5,7 @@
 #include <cudaTypedefs.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -233,6 +234,10 @@ tcfftResult create(tcfftHandle* out, int dims, int nx, int ny, int batch) {
     k.tw4_total = p.tw4_total;
     k.tw4_s = p.N / p.st[p.S - 1].R;
     k.tw4_nk = k.tw4_s;
+    // gather-ahead shifts when each CTA's stores land; the four-step passes
+    // write 16-byte runs whose L2 merging is timing sensitive: keep them lockstep
+    k.gather_ahead = (p.tw4_total || p.kind == tcfft::kPassRowT) ? 0 : 1;
+    if (const char* e = std::getenv("TCFFT_GATHER_AHEAD")) k.gather_ahead = std::atoi(e);
     cudaFuncSetAttribute(d.k->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, p.smem_bytes);
     int64_t slots = (int64_t)prop.multiProcessorCount * p.ctas_per_sm;
     d.grid = (int)std::min<int64_t>(p.chunks, slots);
