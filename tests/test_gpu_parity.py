@@ -201,3 +201,20 @@ def test_execute_host_matches_device_path(nx, ny, batch):
     assert torch.equal(ho.view(torch.int16), y.cpu().view(torch.int16))
     tc.execute_host(plan, h)  # in place on the host
     assert torch.equal(h.view(torch.int16), y.cpu().view(torch.int16))
+
+
+@pytest.mark.parametrize("nx,ny,batch", [(512, 512, 64), (256, 256, 128), (1024, 1024, 32)])
+def test_2d_fused_single_launch_matches_two_pass(nx, ny, batch, monkeypatch):
+    """Opt-in fused 2D kernel (TCFFT_FUSED=1: rows + columns in one persistent
+    launch over L2-sized image groups) is bit-identical to the two-launch path."""
+    tc = _tc()
+    g = torch.Generator(device="cuda").manual_seed(5)
+    x = (torch.rand((batch, nx * ny, 2), device="cuda", generator=g) * 2 - 1).half()
+    y2 = torch.empty_like(x)
+    tc.execute(tc.plan_2d(nx, ny, batch), x, out=y2)
+    monkeypatch.setenv("TCFFT_FUSED", "1")
+    monkeypatch.setenv("TCFFT_FUSED_MB", "2")
+    y1 = torch.empty_like(x)
+    tc.execute(tc.plan_2d(nx, ny, batch), x, out=y1)
+    torch.cuda.synchronize()
+    assert torch.equal(y1.view(torch.int16), y2.view(torch.int16))
