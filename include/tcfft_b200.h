@@ -61,6 +61,12 @@ tcfftResult tcfftExecC2C(tcfftHandle plan, const void* idata, void* odata);
  * may alias.  Ordered after prior work on the plan's stream; completion is
  * ordered before later work on it (synchronize the stream before reading hout). */
 tcfftResult tcfftExecC2CHost(tcfftHandle plan, const void* hin, void* hout);
+/* Strided views (reference BatchedTensor, executor.py:25-51): element j of
+ * transform b at idata[b*batch_stride + j*stride] (complex elements), same for
+ * odata; 2D plans require stride 1.  Contiguous and padded-row views run the
+ * transform directly; other views go through a plan-owned contiguous scratch. */
+tcfftResult tcfftExecC2CStrided(tcfftHandle plan, const void* idata, void* odata, long long stride,
+                                long long batch_stride);
 tcfftResult tcfftDestroy(tcfftHandle plan);
 
 const char* tcfftGetErrorString(tcfftResult r);

@@ -209,6 +209,10 @@ def execute(plan: Plan, data, out=None, stream=None):
 
     if plan._handle is None:
         raise ExecuteError("plan has been destroyed")
+    from .tensor import BatchedTensor
+
+    if isinstance(data, BatchedTensor):
+        return _execute_view(plan, data, stream)
     t, n = _as_pairs(data)
     if n != plan.batch * plan.n_logical:
         raise ExecuteError(f"data holds {n} complex elements, plan needs batch={plan.batch} x "
@@ -230,6 +234,30 @@ def execute(plan: Plan, data, out=None, stream=None):
     if st != _lib.TCFFT_SUCCESS:
         raise ExecuteError(f"tcfftExecC2C failed: {_lib.error_string(st)}")
     return o if out is not None else data
+
+
+def _execute_view(plan: Plan, data, stream=None):
+    """In-place transform of a strided BatchedTensor view (executor.py:152-190)."""
+    import torch
+
+    if data.length != plan.n_logical or data.batch != plan.batch:
+        raise ExecuteError(f"data shape (batch={data.batch}, len={data.length}) does not match plan "
+                           f"(batch={plan.batch}, len={plan.n_logical})")
+    if plan.dims == 2 and data.stride != 1:
+        raise ExecuteError("2D execution requires contiguous row-major data")
+    t = data.pairs
+    if not t.is_cuda or t.dtype != torch.float16 or not t.is_contiguous():
+        raise ExecuteError("BatchedTensor pairs must be a contiguous float16 CUDA tensor")
+    L = _lib.load()
+    s = stream if stream is not None else torch.cuda.current_stream(t.device)
+    with torch.cuda.device(t.device):
+        st = L.tcfftSetStream(plan._handle, ctypes.c_void_p(s.cuda_stream))
+        if st == _lib.TCFFT_SUCCESS:
+            ptr = ctypes.c_void_p(t.data_ptr())
+            st = L.tcfftExecC2CStrided(plan._handle, ptr, ptr, data.stride, data.batch_stride)
+    if st != _lib.TCFFT_SUCCESS:
+        raise ExecuteError(f"tcfftExecC2CStrided failed: {_lib.error_string(st)}")
+    return data
 
 
 def execute_host(plan: Plan, data, out=None, stream=None):
@@ -266,7 +294,11 @@ def flops_5nlogn(n_total: int, batch: int) -> float:
     return 5.0 * n_total * math.log2(n_total) * batch
 
 
+from .tcf import read_tcf, write_tcf  # noqa: E402  (TCF1 files, executor.py:203-230)
+from .tensor import BatchedTensor  # noqa: E402  (strided views, executor.py:25-74)
+
 __all__ = [
+    "BatchedTensor", "read_tcf", "write_tcf",
     "ExecuteError", "Plan", "PlanArgumentError", "UnsupportedSizeError", "execute", "execute_host", "flops_5nlogn",
     "plan_1d", "plan_2d", "schedule_radices",
 ]

@@ -27,6 +27,7 @@ TCFFT_NO_DEVICE = 7
 # every symbol include/tcfft_b200.h declares
 EXPORTS = (
     "tcfftPlan1D", "tcfftPlan2D", "tcfftSetStream", "tcfftGetWorkspaceSize", "tcfftExecC2C", "tcfftExecC2CHost",
+    "tcfftExecC2CStrided",
     "tcfftDestroy", "tcfftGetErrorString", "tcfftGetVersion", "tcfftDescribePlan", "tcfftPlanTables",
 )
 
@@ -54,6 +55,8 @@ def load(build_if_missing: bool = True):
     L.tcfftSetStream.argtypes = [vp, vp]
     L.tcfftGetWorkspaceSize.argtypes = [vp, ctypes.POINTER(sz)]
     L.tcfftExecC2C.argtypes = [vp, vp, vp]
+    if hasattr(L, "tcfftExecC2CStrided"):
+        L.tcfftExecC2CStrided.argtypes = [vp, vp, vp, ctypes.c_longlong, ctypes.c_longlong]
     if hasattr(L, "tcfftExecC2CHost"):
         L.tcfftExecC2CHost.argtypes = [vp, vp, vp]
     L.tcfftDestroy.argtypes = [vp]

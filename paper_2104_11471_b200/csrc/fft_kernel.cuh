@@ -33,6 +33,7 @@ struct KIo {
   int32_t box_rows, n_sub, sub_bytes, chunk_rows;
   int32_t C, spi;       // box: columns per chunk, chunks per image
   int32_t pitch_bytes;  // pitch mode: staging pitch per transform
+  int64_t gstride_bytes;  // pitch mode: global distance between transforms (batch_stride * 4)
   int64_t count;        // pitch mode: transforms in the pass
   const uint8_t* gptr;  // pitch mode: raw global pointer, set per execution
 };
@@ -312,7 +313,8 @@ DEVI void issue_load(const CUtensorMap* tm, const KIo& io, int T, int64_t chunk,
     const int64_t t0 = chunk * T;
     const int nt = (int)min((int64_t)T, io.count - t0);
     mbar_arrive_expect_tx(bar, (uint32_t)(nt * io.sub_bytes));
-    for (int i = 0; i < nt; ++i) bulk_g2s(dst + i * io.pitch_bytes, io.gptr + (t0 + i) * io.sub_bytes, io.sub_bytes, bar);
+    for (int i = 0; i < nt; ++i)
+      bulk_g2s(dst + i * io.pitch_bytes, io.gptr + (t0 + i) * io.gstride_bytes, io.sub_bytes, bar);
     return;
   }
   mbar_arrive_expect_tx(bar, (uint32_t)(io.n_sub * io.sub_bytes));
@@ -339,7 +341,7 @@ DEVI void issue_store(const CUtensorMap* tm, const KIo& io, int T, int64_t chunk
     const int64_t t0 = chunk * T;
     const int nt = (int)min((int64_t)T, io.count - t0);
     for (int i = 0; i < nt; ++i)
-      bulk_s2g(const_cast<uint8_t*>(io.gptr) + (t0 + i) * io.sub_bytes, src + i * io.pitch_bytes, io.sub_bytes);
+      bulk_s2g(const_cast<uint8_t*>(io.gptr) + (t0 + i) * io.gstride_bytes, src + i * io.pitch_bytes, io.sub_bytes);
   } else if (io.mode == kIoRank1) {
     const int32_t e0 = (int32_t)(chunk * io.chunk_rows);
     for (int i = 0; i < io.n_sub; ++i) tma_store_1d(tm, e0 + i * io.box_rows, src + i * io.sub_bytes);

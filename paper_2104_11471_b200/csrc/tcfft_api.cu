@@ -161,6 +161,8 @@ struct tcfftPlanImpl {
   FusedState fused;
   void* ws = nullptr;
   HostPipe* pipe = nullptr;  // lazily built by tcfftExecC2CHost
+  void* scratch = nullptr;   // strided views: contiguous staging (lazy)
+  size_t scratch_bytes = 0;
   cudaStream_t stream = nullptr;
   int device = 0;
   int magic = 0x7cff7;
@@ -217,6 +219,7 @@ tcfft::KIo to_kio(const tcfft::IoDesc& io, const PassPlan& p) {
   k.C = io.C;
   k.spi = io.spi;
   k.pitch_bytes = p.pitch * 4;
+  k.gstride_bytes = (int64_t)io.sub_bytes;  // contiguous transforms; strided exec overrides
   k.count = p.count;
   return k;
 }
@@ -580,11 +583,80 @@ extern "C" tcfftResult tcfftExecC2CHost(tcfftHandle plan, const void* hin, void*
   return cudaGetLastError() == cudaSuccess ? TCFFT_SUCCESS : TCFFT_EXEC_FAILED;
 }
 
+// ---------------------------------------------------------------------------
+// Strided 1D views (reference BatchedTensor, executor.py:25-51): element j of
+// transform b at idata[b*batch_stride + j*stride] (complex elements).
+//   stride 1, batch_stride == N          : contiguous fast path
+//   stride 1, padded batch_stride (x4)   : per-transform bulk copies straight
+//                                          from the padded rows (64 <= N <= 1024)
+//   anything else                        : gather into a contiguous scratch,
+//                                          transform, scatter back
+__global__ void strided_copy_kernel(const uint32_t* __restrict__ src, uint32_t* __restrict__ dst, int64_t batch,
+                                    int64_t n, int64_t stride, int64_t bstride, int to_contig) {
+  const int64_t total = batch * n;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = i / n, j = i - b * n;
+    const int64_t s = b * bstride + j * stride;
+    if (to_contig)
+      dst[i] = src[s];
+    else
+      dst[s] = src[i];
+  }
+}
+
+extern "C" tcfftResult tcfftExecC2CStrided(tcfftHandle plan, const void* idata, void* odata, long long stride,
+                                           long long batch_stride) {
+  if (!valid(plan)) return TCFFT_INVALID_PLAN;
+  const tcfft::Plan& P = plan->plan;
+  const int64_t n = (int64_t)P.nx * (P.dims == 2 ? P.ny : 1);
+  if (stride < 1 || (P.batch > 1 && batch_stride < stride * n) || batch_stride < 1) return TCFFT_INVALID_VALUE;
+  if (P.dims == 2 && stride != 1) return TCFFT_INVALID_VALUE;  // executor.py:180-181
+  if (stride == 1 && batch_stride == n) return tcfftExecC2C(plan, idata, odata);
+  if ((reinterpret_cast<uintptr_t>(idata) | reinterpret_cast<uintptr_t>(odata)) & 15) return TCFFT_INVALID_VALUE;
+  if (P.dims == 1 && stride == 1 && (batch_stride % 4) == 0 && plan->dev.size() == 1 &&
+      P.passes[0].in.mode == tcfft::kIoPitch) {
+    const PassPlan& p = P.passes[0];
+    const DevPass& d = plan->dev[0];
+    CUtensorMap t0, t1;
+    std::memset(&t0, 0, sizeof(t0));
+    std::memset(&t1, 0, sizeof(t1));
+    KParams kp = d.kp;
+    kp.in.gptr = static_cast<const uint8_t*>(idata);
+    kp.out.gptr = static_cast<const uint8_t*>(odata);
+    kp.in.gstride_bytes = kp.out.gstride_bytes = batch_stride * 4;
+    d.k->launch(dim3(d.grid), p.smem_bytes, plan->stream, t0, t1, kp);
+    return cudaGetLastError() == cudaSuccess ? TCFFT_SUCCESS : TCFFT_EXEC_FAILED;
+  }
+  // general view: gather -> contiguous transform -> scatter
+  const size_t bytes = (size_t)(P.batch * n * 4);
+  if (plan->scratch_bytes < bytes) {
+    if (plan->scratch) cudaFree(plan->scratch);
+    plan->scratch = nullptr;
+    plan->scratch_bytes = 0;
+    if (cudaMalloc(&plan->scratch, bytes) != cudaSuccess) {
+      cudaGetLastError();
+      return TCFFT_ALLOC_FAILED;
+    }
+    plan->scratch_bytes = bytes;
+  }
+  const int threads = 256, blocks = (int)std::min<int64_t>((P.batch * n + threads - 1) / threads, 148 * 16);
+  strided_copy_kernel<<<blocks, threads, 0, plan->stream>>>(static_cast<const uint32_t*>(idata),
+                                                              static_cast<uint32_t*>(plan->scratch), P.batch, n,
+                                                              stride, batch_stride, 1);
+  tcfftResult st = tcfftExecC2C(plan, plan->scratch, plan->scratch);
+  if (st != TCFFT_SUCCESS) return st;
+  strided_copy_kernel<<<blocks, threads, 0, plan->stream>>>(static_cast<const uint32_t*>(plan->scratch),
+                                                              static_cast<uint32_t*>(odata), P.batch, n, stride,
+                                                              batch_stride, 0);
+  return cudaGetLastError() == cudaSuccess ? TCFFT_SUCCESS : TCFFT_EXEC_FAILED;
+}
+
 tcfftResult tcfftDestroy(tcfftHandle plan) {
   if (!valid(plan)) return TCFFT_INVALID_PLAN;
   for (auto& q : plan->dev) cudaFree(q.tables);
   if (plan->ws) cudaFree(plan->ws);
   if (plan->fused.counters) cudaFree(plan->fused.counters);
+  if (plan->scratch) cudaFree(plan->scratch);
   destroy_pipe(plan->pipe);
   plan->magic = 0;
   delete plan;

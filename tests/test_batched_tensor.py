@@ -1,0 +1,71 @@
+"""BatchedTensor strided views (reference test_executor.py:27-52 and the
+strided-pass tests :168-200)."""
+
+import numpy as np
+import pytest
+
+from oracle import restate as R
+
+torch = pytest.importorskip("torch")
+import paper_2104_11471_b200 as tc  # noqa: E402
+
+
+def test_tensor_rejects_bad_pair_shape():
+    with pytest.raises(tc.ExecuteError):
+        tc.BatchedTensor(torch.zeros((8, 3), dtype=torch.float16), 1, 8)
+
+
+def test_tensor_rejects_short_buffer():
+    with pytest.raises(tc.ExecuteError):
+        tc.BatchedTensor(torch.zeros((7, 2), dtype=torch.float16), 1, 8)
+
+
+def test_tensor_rejects_aliasing_batches():
+    with pytest.raises(tc.ExecuteError):
+        tc.BatchedTensor(torch.zeros((16, 2), dtype=torch.float16), 2, 8, batch_stride=4)
+
+
+def test_tensor_strided_view_addresses():
+    data = tc.BatchedTensor(torch.zeros((64, 2), dtype=torch.float16), 2, 4, stride=8, batch_stride=32)
+    assert data.offsets().tolist() == [0, 32]
+
+
+def test_tensor_complex_round_trip_cpu():
+    z = np.array([[0.5 + 0.25j, -1.0, 2.0j]])
+    d = tc.BatchedTensor.from_complex(z, device="cpu")
+    assert np.array_equal(d.to_complex(), z)
+
+
+def _strided_case(n, batch, stride, bstride, seed):
+    x = R.random_pairs([seed, n], batch, n)  # logical sequences
+    total = bstride * (batch - 1) + stride * (n - 1) + 1
+    buf = np.full((total + 5, 2), np.float16(7.0))  # sentinel outside the view
+    idx = (np.arange(batch)[:, None] * bstride + np.arange(n)[None, :] * stride)
+    buf[idx] = x
+    return x, buf, idx
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,batch,stride,bstride", [(256, 8, 1, 256), (256, 8, 1, 260), (1024, 3, 1, 1100),
+                                                      (512, 4, 3, 2000), (4, 2, 8, 32), (4096, 4, 2, 8195),
+                                                      (1 << 15, 2, 1, (1 << 15) + 16)])
+def test_strided_views_equal_contiguous(n, batch, stride, bstride):
+    x, buf, idx = _strided_case(n, batch, stride, bstride, 3)
+    t = torch.from_numpy(buf).cuda()
+    view = tc.BatchedTensor(t, batch, n, stride=stride, batch_stride=bstride)
+    tc.execute(tc.plan_1d(n, batch), view)
+    got = t.cpu().numpy()
+    y = torch.from_numpy(np.ascontiguousarray(x)).cuda()
+    tc.execute(tc.plan_1d(n, batch), y)
+    want = y.cpu().numpy()
+    assert np.array_equal(got[idx].view(np.uint16), want.view(np.uint16))
+    mask = np.ones(len(buf), bool)
+    mask[idx.reshape(-1)] = False
+    assert np.all(got[mask] == np.float16(7.0))  # nothing outside the view touched
+
+
+def test_interleaved_view_aliases_like_reference():
+    # the reference forbids batch_stride < stride*length for batch > 1
+    # (executor.py:45-46); interleaved columns are the 2D column pass instead
+    with pytest.raises(tc.ExecuteError):
+        tc.BatchedTensor(torch.zeros((64, 2), dtype=torch.float16), 4, 16, stride=4, batch_stride=1)
