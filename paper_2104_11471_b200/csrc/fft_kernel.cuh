@@ -393,6 +393,10 @@ __global__ void __launch_bounds__(128, MINB)
   using C = Cfg<E, R1, R2, R3, MODE>;
   constexpr int S = C::S;
   constexpr int TM = C::TMAX;
+  // Four-step passes write 16-byte runs whose merging in L2 is sensitive to
+  // store timing: they keep the simple (lock-step) chunk loop, measured 1.6x
+  // faster for them than the pipelined loop below (round 1).
+  constexpr bool PIPE = !(TW4 || MODE == kModeRowT);
 
 #ifndef TCFFT_NO_ALIGN_SLACK
   extern __shared__ uint8_t smem_raw[];
@@ -414,7 +418,7 @@ __global__ void __launch_bounds__(128, MINB)
   if (warp == 0) tmem_alloc<C::COLS>(s_tmem);
   if (tid == 0) {
     mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 2);  // tcgen05.commit + thread 0's arrive
+    mbar_init(&bars[1], PIPE ? 2 : 1);  // tcgen05.commit (+ thread 0's arrive when pipelined)
     fence_mbar_init();
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_in) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_out) : "memory");
@@ -489,6 +493,127 @@ __global__ void __launch_bounds__(128, MINB)
 
   float2* s_tw4 = reinterpret_cast<float2*>(smem + p.smem_tw4);
 
+  if constexpr (!PIPE) {
+    // ------------------------------------------------------------ simple loop
+    int64_t chunk = blockIdx.x;
+    if (tid == 0 && chunk < p.chunks) issue_load(&tm_in, p.in, p.T, chunk, s_in, &bars[0]);
+    uint32_t ld_phase = 0, mma_phase = 0;
+    uint8_t* const s_a = smem + p.smem_a;
+    const uint32_t s_a_u = smem_u32(s_a);
+    for (; chunk < p.chunks; chunk += gridDim.x) {
+      if constexpr (TW4) {
+        // four-step twiddle, strip-base part: A[k] = W_Ntot^{base k}, r = W_Ntot^{base s}
+        const int64_t base = (chunk % p.in.spi) * (int64_t)p.in.C;
+        for (int kk = tid; kk <= p.tw4_nk; kk += 128) {
+          const int64_t e = (base * (kk < p.tw4_nk ? kk : p.tw4_s)) % p.tw4_total;
+          float sn, cs;
+          sincospif(-2.0f * (float)e / (float)p.tw4_total, &sn, &cs);
+          s_tw4[kk] = make_float2(cs, sn);
+        }
+      }
+      mbar_wait(&bars[0], ld_phase);
+      ld_phase ^= 1;
+      int g1[C::T(0)];
+      if constexpr (RT) {
+        tmem_ld_words<C::T(0)>(tR, reinterpret_cast<uint32_t*>(g1));
+        tmem_wait_ld();
+      } else {
+#pragma unroll
+        for (int t = 0; t < C::T(0); ++t) g1[t] = gb[t];
+      }
+#pragma unroll
+      for (int t = 0; t < C::T(0); ++t)
+        gather_to_tmem<C>(s_in_u, g1[t], p.gstride, (uint32_t)p.swz_in, tA + lane_off + t * (C::KP(0) / 2));
+      tmem_wait_st();
+      tc_fence_before();
+      __syncthreads();
+      if (tid == 0) {
+        tc_fence_after();
+        const int64_t nxt = chunk + gridDim.x;
+        if (nxt < p.chunks) issue_load(&tm_in, p.in, p.T, nxt, s_in, &bars[0]);  // staging buffer is free again
+        bulk_wait_read0();  // previous chunk's output store no longer reads s_a
+        issue_stage_mma<C, 0>(s_a_u, s_b_u, tD, tA);
+        mma_commit(&bars[1]);
+      }
+      mbar_wait(&bars[1], mma_phase);
+      mma_phase ^= 1;
+      tc_fence_after();
+      auto writer = [&](auto sc) {
+        constexpr int s = decltype(sc)::value;
+        [[maybe_unused]] uint32_t rw[C::T(s) * RC::WS(s)];
+        if constexpr (RT) {
+          tmem_ld_words<C::T(s) * RC::WS(s)>(tR + RC::OFF_W(s), rw);
+          tmem_wait_ld();
+        }
+#pragma unroll
+        for (int t = 0; t < C::T(s); ++t) {
+          int ad;
+          float2 cc = make_float2(1.f, 0.f), wv;
+          if constexpr (RT) {
+            const uint32_t* q = rw + t * RC::WS(s);
+            ad = (int)q[0];
+            wv = make_float2(__uint_as_float(q[1]), __uint_as_float(q[2]));
+            if constexpr (s >= 1) cc = make_float2(__uint_as_float(q[3]), __uint_as_float(q[4]));
+          } else {
+            ad = waddr[s][t];
+            wv = ww[s][t];
+            if constexpr (s >= 1) cc = wc[s][t];
+          }
+          writer_epilogue<C, s>(tD + lane_off + t * C::NP(s), s_a_u + ad, cc, wv);
+        }
+        fence_proxy_async_smem();
+        tc_fence_before();
+        __syncthreads();
+        if (tid == 0) {
+          tc_fence_after();
+          issue_stage_mma<C, s + 1>(s_a_u, s_b_u, tD, tA);
+          mma_commit(&bars[1]);
+        }
+        mbar_wait(&bars[1], mma_phase);
+        mma_phase ^= 1;
+        tc_fence_after();
+      };
+      if constexpr (S >= 2) writer(std::integral_constant<int, 0>{});
+      if constexpr (S >= 3) writer(std::integral_constant<int, 1>{});
+      [[maybe_unused]] uint32_t rf[C::T(S - 1) * RC::FW];
+      if constexpr (RT) {
+        tmem_ld_words<C::T(S - 1) * RC::FW>(tR + RC::OFF_F, rf);
+        tmem_wait_ld();
+      }
+#pragma unroll
+      for (int t = 0; t < C::T(S - 1); ++t) {
+        float2 c4 = make_float2(1.f, 0.f), w4 = make_float2(1.f, 0.f);
+        int ad;
+        if constexpr (RT)
+          ad = (int)rf[t * RC::FW];
+        else
+          ad = waddr[S - 1][t];
+        if constexpr (TW4) {
+          int kk;
+          float2 hc, hw;
+          if constexpr (RT) {
+            const uint32_t* q = rf + t * RC::FW;
+            kk = (int)q[1];
+            hc = make_float2(__uint_as_float(q[2]), __uint_as_float(q[3]));
+            hw = make_float2(__uint_as_float(q[4]), __uint_as_float(q[5]));
+          } else {
+            kk = fk[t];
+            hc = wc[S - 1][t];
+            hw = ww[S - 1][t];
+          }
+          const float2 a = s_tw4[kk], r = s_tw4[p.tw4_nk];
+          c4 = make_float2(a.x * hc.x - a.y * hc.y, a.x * hc.y + a.y * hc.x);
+          w4 = make_float2(r.x * hw.x - r.y * hw.y, r.x * hw.y + r.y * hw.x);
+        }
+        final_epilogue<C, TW4>(tD + lane_off + t * C::NP(S - 1), s_a_u, ad, p.ostride, (uint32_t)p.swz_out, c4,
+                               w4);
+      }
+      fence_proxy_async_smem();
+      tc_fence_before();
+      __syncthreads();
+      if (tid == 0) issue_store(&tm_out, p.out, p.T, chunk, s_a);
+    }
+  } else {
   // ---------------------------------------------------------------------
   // Software-pipelined chunk loop.  The MMA barrier (bars[1]) completes on two
   // arrivals: the tcgen05.commit of the stage's MMAs and a plain arrive by
@@ -652,6 +777,7 @@ __global__ void __launch_bounds__(128, MINB)
       }
     }
   }
+  }  // PIPE
   if (tid == 0) bulk_wait0();
   tc_fence_before();
   __syncthreads();

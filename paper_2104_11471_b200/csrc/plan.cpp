@@ -12,6 +12,7 @@
 
 #include <cmath>
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -106,6 +107,10 @@ std::vector<int> choose_radices(int n) {
 }
 
 int chunk_elems_for(int n) {
+  // experiment hook: TCFFT_CHUNK_<n>=<elems> overrides the chunk size
+  char key[32];
+  std::snprintf(key, sizeof(key), "TCFFT_CHUNK_%d", n);
+  if (const char* e = std::getenv(key)) return std::atoi(e);
   if (n <= 2) return 1024;
   if (n == 4) return 2048;
   if (n <= 4096) return 4096;
@@ -501,12 +506,28 @@ int build_plan(Plan& plan, int dims, int nx, int ny, int64_t batch, std::string*
       return 6;
     }
     const int N1 = 1 << (lg / 2), N2 = 1 << (lg - lg / 2);
+    // The batch is walked in L2-sized groups of G transforms (two launches per
+    // group): the group's workspace (reused by every group) stays resident in
+    // L2, so the intermediate never round-trips HBM and the 16-byte runs of
+    // the transposed / strided accesses merge in L2 before write-back.
+    // (opt-in: measured slower than one ungrouped launch per pass in round 1,
+    // 17.9 vs 18.9 TFLOP/s for C3 at 128 MiB groups with CUDA-graph replay)
+    int64_t group_mb = 0;
+    if (const char* e = std::getenv("TCFFT_FOURSTEP_MB")) group_mb = std::max(0, std::atoi(e));
+    int64_t G = batch;
+    if (group_mb > 0) {
+      G = std::max<int64_t>(1, (group_mb << 20) / ((int64_t)nx * 4));
+      G = std::min<int64_t>(G, batch);
+      while (batch % G) --G;
+    }
     PassPlan p1, p2;
-    if (!build_pass(p1, kPassStrip, N1, 0, batch, N2, err, nx)) return 6;
-    if (!build_pass(p2, kPassRowT, N2, batch * (int64_t)N1, batch, 0, err)) return 6;
+    if (!build_pass(p1, kPassStrip, N1, 0, G, N2, err, nx)) return 6;
+    if (!build_pass(p2, kPassRowT, N2, G * (int64_t)N1, G, 0, err)) return 6;
     p1.ws_out = 1;
     p2.ws_in = 1;
-    plan.ws_bytes = (size_t)batch * (size_t)nx * 4;
+    plan.groups = batch / G;
+    plan.group_bytes = (size_t)G * (size_t)nx * 4;
+    plan.ws_bytes = plan.group_bytes;
     plan.passes.push_back(std::move(p1));
     plan.passes.push_back(std::move(p2));
     return 0;

@@ -110,6 +110,8 @@ struct Plan {
   int32_t nx = 0, ny = 0;
   int64_t batch = 0;
   size_t ws_bytes = 0;
+  int64_t groups = 1;       // passes run once per group of transforms
+  size_t group_bytes = 0;   // input / output bytes of one group
   std::vector<PassPlan> passes;
 };
 

@@ -55,10 +55,12 @@ const KernelEntry kKernels[] = {
     KBOTH(4096, 16, 8, 0, 4),     KBOTH(4096, 16, 16, 0, 4),    KBOTH(4096, 16, 32, 0, 4),
     KBOTH(4096, 32, 32, 0, 4),    KBOTH(4096, 16, 16, 8, 4),    KBOTH(4096, 16, 16, 16, 4),
     KROW(8192, 16, 16, 32, 2),    KSTRIP(8192, 16, 16, 8, 2),   KROW(16384, 16, 32, 32, 1),
+    KROW(8192, 16, 16, 16, 2),    KROW(8192, 16, 32, 0, 2),     KROW(8192, 16, 16, 0, 2),
     KSTRIP(16384, 16, 16, 16, 1),
     // four-step: N1 / N2 in {128 .. 4096}
     KFOUR(4096, 16, 8, 0, 4),     KFOUR(4096, 16, 16, 0, 4),    KFOUR(4096, 16, 32, 0, 4),
     KFOUR(4096, 32, 32, 0, 4),    KFOUR(8192, 16, 16, 8, 2),    KFOUR(16384, 16, 16, 16, 1),
+    KFOUR(16384, 16, 16, 8, 1),
 };
 
 const KernelEntry* find_kernel(const PassPlan& p) {
@@ -163,6 +165,13 @@ struct tcfftPlanImpl {
   HostPipe* pipe = nullptr;  // lazily built by tcfftExecC2CHost
   void* scratch = nullptr;   // strided views: contiguous staging (lazy)
   size_t scratch_bytes = 0;
+  struct GraphEntry {
+    const void* in;
+    void* out;
+    cudaGraphExec_t exec;
+  };
+  std::vector<GraphEntry> graphs;  // grouped plans: cached per (idata, odata)
+  cudaStream_t cap_stream = nullptr;
   cudaStream_t stream = nullptr;
   int device = 0;
   int magic = 0x7cff7;
@@ -408,6 +417,9 @@ bool valid(tcfftHandle h) { return h && h->magic == 0x7cff7; }
 
 }  // namespace
 
+static tcfftResult launch_passes(tcfftHandle plan, const void* idata, void* odata, cudaStream_t st);
+static tcfftResult exec_grouped(tcfftHandle plan, const void* idata, void* odata);
+
 extern "C" {
 
 tcfftResult tcfftPlan1D(tcfftHandle* plan, int nx, int batch) { return create(plan, 1, nx, 0, batch); }
@@ -446,11 +458,21 @@ tcfftResult tcfftExecC2C(tcfftHandle plan, const void* idata, void* odata) {
     plan->fused.k->launch(dim3(plan->fused.grid), plan->fused.smem, plan->stream, a0, a1, b0, b1, f);
     return cudaGetLastError() == cudaSuccess ? TCFFT_SUCCESS : TCFFT_EXEC_FAILED;
   }
-  const void* src = idata;
+  if (plan->plan.groups > 1) return exec_grouped(plan, idata, odata);
+  return launch_passes(plan, idata, odata, plan->stream);
+}
+
+}  // extern "C"
+
+// All pass launches of one execution, on stream `st`.
+static tcfftResult launch_passes(tcfftHandle plan, const void* idata, void* odata, cudaStream_t st) {
+  for (int64_t g = 0; g < plan->plan.groups; ++g) {
+  const size_t goff = (size_t)g * plan->plan.group_bytes;
+  const void* src = static_cast<const char*>(idata) + goff;
   for (size_t i = 0; i < plan->dev.size(); ++i) {
     const PassPlan& p = plan->plan.passes[i];
     const DevPass& d = plan->dev[i];
-    void* dst = p.ws_out ? plan->ws : odata;
+    void* dst = p.ws_out ? plan->ws : static_cast<void*>(static_cast<char*>(odata) + goff);
     if (p.ws_in) src = plan->ws;
     CUtensorMap tin, tout;
     if (make_tmap(&tin, p.in, src) != TCFFT_SUCCESS || make_tmap(&tout, p.out, dst) != TCFFT_SUCCESS)
@@ -458,12 +480,52 @@ tcfftResult tcfftExecC2C(tcfftHandle plan, const void* idata, void* odata) {
     KParams kp = d.kp;
     kp.in.gptr = static_cast<const uint8_t*>(src);
     kp.out.gptr = static_cast<const uint8_t*>(dst);
-    d.k->launch(dim3(d.grid), p.smem_bytes, plan->stream, tin, tout, kp);
+    d.k->launch(dim3(d.grid), p.smem_bytes, st, tin, tout, kp);
     if (cudaGetLastError() != cudaSuccess) return TCFFT_EXEC_FAILED;
     src = dst;
   }
+  }
   return TCFFT_SUCCESS;
 }
+
+// Grouped (L2-resident four-step) plans issue two launches per group: replay
+// them as one CUDA graph, instantiated once per (idata, odata) pair, unless the
+// caller's stream is itself being captured.
+static tcfftResult exec_grouped(tcfftHandle plan, const void* idata, void* odata) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(plan->stream, &cs);
+  if (cs != cudaStreamCaptureStatusNone) return launch_passes(plan, idata, odata, plan->stream);
+  for (auto& e : plan->graphs)
+    if (e.in == idata && e.out == odata) {
+      return cudaGraphLaunch(e.exec, plan->stream) == cudaSuccess ? TCFFT_SUCCESS : TCFFT_EXEC_FAILED;
+    }
+  if (!plan->cap_stream && cudaStreamCreateWithFlags(&plan->cap_stream, cudaStreamNonBlocking) != cudaSuccess)
+    return TCFFT_EXEC_FAILED;
+  cudaGraph_t g = nullptr;
+  if (cudaStreamBeginCapture(plan->cap_stream, cudaStreamCaptureModeThreadLocal) != cudaSuccess)
+    return TCFFT_EXEC_FAILED;
+  tcfftResult r = launch_passes(plan, idata, odata, plan->cap_stream);
+  if (cudaStreamEndCapture(plan->cap_stream, &g) != cudaSuccess || r != TCFFT_SUCCESS) {
+    if (g) cudaGraphDestroy(g);
+    cudaGetLastError();
+    return TCFFT_EXEC_FAILED;
+  }
+  cudaGraphExec_t ex = nullptr;
+  if (cudaGraphInstantiate(&ex, g, 0) != cudaSuccess) {
+    cudaGraphDestroy(g);
+    cudaGetLastError();
+    return TCFFT_EXEC_FAILED;
+  }
+  cudaGraphDestroy(g);
+  if (plan->graphs.size() >= 4) {
+    cudaGraphExecDestroy(plan->graphs.front().exec);
+    plan->graphs.erase(plan->graphs.begin());
+  }
+  plan->graphs.push_back({idata, odata, ex});
+  return cudaGraphLaunch(ex, plan->stream) == cudaSuccess ? TCFFT_SUCCESS : TCFFT_EXEC_FAILED;
+}
+
+extern "C" {
 
 // ---------------------------------------------------------------------------
 // Host-buffer execution: the batch is cut into slices of whole transforms;
@@ -505,7 +567,8 @@ static tcfftResult build_pipe(tcfftHandle plan) {
   const int64_t bytes_per = n * 4;
   auto* hp = new (std::nothrow) HostPipe();
   if (!hp) return TCFFT_ALLOC_FAILED;
-  const int64_t target = 32ll << 20;  // ~32 MiB slices
+  int64_t target = 16ll << 20;  // ~16 MiB slices (measured best of 8..128 MiB for C2)
+  if (const char* e = std::getenv("TCFFT_SLICE_MB")) target = std::max(1, std::atoi(e)) * (1ll << 20);
   hp->slice_batch = std::max<int64_t>(1, std::min<int64_t>(P.batch, target / bytes_per));
   hp->slices = (P.batch + hp->slice_batch - 1) / hp->slice_batch;
   hp->tail = P.batch - (hp->slices - 1) * hp->slice_batch;
@@ -631,6 +694,8 @@ extern "C" tcfftResult tcfftExecC2CStrided(tcfftHandle plan, const void* idata, 
   const size_t bytes = (size_t)(P.batch * n * 4);
   if (plan->scratch_bytes < bytes) {
     if (plan->scratch) cudaFree(plan->scratch);
+  for (auto& e : plan->graphs) cudaGraphExecDestroy(e.exec);
+  if (plan->cap_stream) cudaStreamDestroy(plan->cap_stream);
     plan->scratch = nullptr;
     plan->scratch_bytes = 0;
     if (cudaMalloc(&plan->scratch, bytes) != cudaSuccess) {
@@ -657,6 +722,8 @@ tcfftResult tcfftDestroy(tcfftHandle plan) {
   if (plan->ws) cudaFree(plan->ws);
   if (plan->fused.counters) cudaFree(plan->fused.counters);
   if (plan->scratch) cudaFree(plan->scratch);
+  for (auto& e : plan->graphs) cudaGraphExecDestroy(e.exec);
+  if (plan->cap_stream) cudaStreamDestroy(plan->cap_stream);
   destroy_pipe(plan->pipe);
   plan->magic = 0;
   delete plan;
@@ -689,7 +756,7 @@ tcfftResult tcfftDescribePlan(int dims, int nx, int ny, int batch, char* json, s
   } else {
     s = "{\"dims\": " + std::to_string(dims) + ", \"nx\": " + std::to_string(nx) + ", \"ny\": " +
         std::to_string(ny) + ", \"batch\": " + std::to_string(batch) + ", \"ws_bytes\": " +
-        std::to_string(plan.ws_bytes) + ", \"passes\": [";
+        std::to_string(plan.ws_bytes) + ", \"groups\": " + std::to_string(plan.groups) + ", \"passes\": [";
     for (size_t i = 0; i < plan.passes.size(); ++i) {
       const PassPlan& p = plan.passes[i];
       if (i) s += ", ";
