@@ -52,6 +52,10 @@ struct KParams {
   int32_t tw4_nk;     // number of final-stage k values (N1 / R_S)
   int32_t tw4_s;      // N1 / R_S
   int32_t gather_ahead;  // gather chunk i+1 while chunk i's last MMAs run
+  int32_t pipe;          // software-pipelined chunk loop (else the simple lock-step loop)
+  int32_t pdl;           // PDL trigger point: 1 = last chunk, 2 = CTA start
+  unsigned long long* trace;  // TCFFT_TRACE builds: per-CTA globaltimer stamps
+  unsigned long long* ctr;    // dynamic chunk tickets {next, retired CTAs}; null = static
 };
 
 namespace dev {
@@ -396,7 +400,17 @@ __global__ void __launch_bounds__(128, MINB)
   // Four-step passes write 16-byte runs whose merging in L2 is sensitive to
   // store timing: they keep the simple (lock-step) chunk loop, measured 1.6x
   // faster for them than the pipelined loop below (round 1).
-  constexpr bool PIPE = !(TW4 || MODE == kModeRowT);
+  constexpr bool PIPE_OK = !(TW4 || MODE == kModeRowT) && S >= 2;
+  const bool PIPE = PIPE_OK && p.pipe;
+  // Chunk schedule: a CTA's first chunk is blockIdx.x; later ones come from a
+  // global ticket counter (thread 0, in load order), so CTAs on slower SMs
+  // simply take fewer chunks (static striding left a 15 us tail on C2).  The
+  // last CTA to retire resets the counter for the next launch.
+  auto next_chunk = [&](int64_t cur) -> int64_t {
+    if (!p.ctr) return cur + gridDim.x;
+    const int64_t c = (int64_t)gridDim.x + (int64_t)atomicAdd(p.ctr, 1ull);
+    return c < p.chunks ? c : p.chunks;
+  };
 
 #ifndef TCFFT_NO_ALIGN_SLACK
   extern __shared__ uint8_t smem_raw[];
@@ -409,12 +423,17 @@ __global__ void __launch_bounds__(128, MINB)
   uint8_t* s_b = smem + p.smem_b;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.smem_bar);
   uint32_t* s_tmem = reinterpret_cast<uint32_t*>(bars + 2);
+  int64_t* s_q = reinterpret_cast<int64_t*>(bars + 4);  // chunk ids in load order (ring of 4)
   const int tid = threadIdx.x, warp = tid >> 5;
   const uint32_t s_in_u = smem_u32(s_in), s_b_u = smem_u32(s_b);
 
-  // constants: B matrices, once per CTA
-  for (int i = tid; i < p.bbytes / 16; i += 128)
-    reinterpret_cast<uint4*>(s_b)[i] = reinterpret_cast<const uint4*>(p.bblob)[i];
+  // Thread 0 starts the first chunk's TMA load before anything else; the
+  // other threads meanwhile stage the plan constants (B matrices, row
+  // records).  Only thread 0 touches the transform's input/output (all data
+  // movement is TMA), so only it waits on the preceding grid (PDL).
+  // PDL trigger: at CTA start (pdl == 2), else as the CTA takes its last chunk
+  if (p.pdl == 2 || (int64_t)blockIdx.x + gridDim.x >= p.chunks) griddep_launch_dependents();
+  bool triggered = p.pdl == 2 || (int64_t)blockIdx.x + gridDim.x >= p.chunks;
   if (warp == 0) tmem_alloc<C::COLS>(s_tmem);
   if (tid == 0) {
     mbar_init(&bars[0], 1);
@@ -422,7 +441,18 @@ __global__ void __launch_bounds__(128, MINB)
     fence_mbar_init();
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_in) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_out) : "memory");
+#ifdef TCFFT_TRACE
+    if (p.trace) p.trace[blockIdx.x * 4 + 0] = globaltimer_ns();
+#endif
+    griddep_wait();
+#ifdef TCFFT_TRACE
+    if (p.trace) p.trace[blockIdx.x * 4 + 1] = globaltimer_ns();
+#endif
+    if ((int64_t)blockIdx.x < p.chunks) issue_load(&tm_in, p.in, p.T, (int64_t)blockIdx.x, s_in, &bars[0]);
   }
+  // constants: B matrices, once per CTA
+  for (int i = tid; i < p.bbytes / 16; i += 128)
+    reinterpret_cast<uint4*>(s_b)[i] = reinterpret_cast<const uint4*>(p.bblob)[i];
 
   // per-thread row records (host-built, see plan.cpp)
   auto rec = [&](int s, int t) -> const RowInfo& { return p.rows_tab[((size_t)s * p.tiles_max + t) * 128 + tid]; };
@@ -493,14 +523,13 @@ __global__ void __launch_bounds__(128, MINB)
 
   float2* s_tw4 = reinterpret_cast<float2*>(smem + p.smem_tw4);
 
-  if constexpr (!PIPE) {
+  if (!PIPE) {
     // ------------------------------------------------------------ simple loop
-    int64_t chunk = blockIdx.x;
-    if (tid == 0 && chunk < p.chunks) issue_load(&tm_in, p.in, p.T, chunk, s_in, &bars[0]);
+    int64_t chunk = blockIdx.x;  // its load was issued in the prologue
     uint32_t ld_phase = 0, mma_phase = 0;
     uint8_t* const s_a = smem + p.smem_a;
     const uint32_t s_a_u = smem_u32(s_a);
-    for (; chunk < p.chunks; chunk += gridDim.x) {
+    while (chunk < p.chunks) {
       if constexpr (TW4) {
         // four-step twiddle, strip-base part: A[k] = W_Ntot^{base k}, r = W_Ntot^{base s}
         const int64_t base = (chunk % p.in.spi) * (int64_t)p.in.C;
@@ -529,8 +558,10 @@ __global__ void __launch_bounds__(128, MINB)
       __syncthreads();
       if (tid == 0) {
         tc_fence_after();
-        const int64_t nxt = chunk + gridDim.x;
+        const int64_t nxt = next_chunk(chunk);
+        s_q[0] = nxt;  // read by all threads after this iteration's last barrier
         if (nxt < p.chunks) issue_load(&tm_in, p.in, p.T, nxt, s_in, &bars[0]);  // staging buffer is free again
+        else if (p.pdl == 1 && !triggered) griddep_launch_dependents();  // this CTA's last chunk
         bulk_wait_read0();  // previous chunk's output store no longer reads s_a
         issue_stage_mma<C, 0>(s_a_u, s_b_u, tD, tA);
         mma_commit(&bars[1]);
@@ -612,8 +643,9 @@ __global__ void __launch_bounds__(128, MINB)
       tc_fence_before();
       __syncthreads();
       if (tid == 0) issue_store(&tm_out, p.out, p.T, chunk, s_a);
+      chunk = s_q[0];
     }
-  } else {
+  } else if constexpr (PIPE_OK) {
   // ---------------------------------------------------------------------
   // Software-pipelined chunk loop.  The MMA barrier (bars[1]) completes on two
   // arrivals: the tcgen05.commit of the stage's MMAs and a plain arrive by
@@ -663,24 +695,27 @@ __global__ void __launch_bounds__(128, MINB)
   uint8_t* const s_a = smem + p.smem_a;
   const uint32_t s_a_u = smem_u32(s_a);
 
-  if (chunk0 < p.chunks) {
-    if (tid == 0) issue_load(&tm_in, p.in, p.T, chunk0, s_in, &bars[0]);
+  if (chunk0 < p.chunks) {  // its load was issued in the prologue
     gather();
     tc_fence_before();
     __syncthreads();
     if (tid == 0) {
       tc_fence_after();
-      if (chunk0 + gridDim.x < p.chunks) issue_load(&tm_in, p.in, p.T, chunk0 + gridDim.x, s_in, &bars[0]);
+      const int64_t c1 = next_chunk(chunk0);
+      s_q[1] = c1;  // read after the first writer barrier of iteration 0
+      if (c1 < p.chunks) issue_load(&tm_in, p.in, p.T, c1, s_in, &bars[0]);
+      else if (p.pdl == 1 && !triggered) griddep_launch_dependents();
       issue_stage_mma<C, 0>(s_a_u, s_b_u, tD, tA);
       mma_commit(&bars[1]);
       mbar_arrive(&bars[1]);
     }
   }
 
-  for (int64_t chunk = chunk0; chunk < p.chunks; chunk += gridDim.x) {
-    const int64_t next = chunk + gridDim.x;
-    const bool has_next = next < p.chunks;
+  int64_t chunk = chunk0;
+  for (int it = 0; chunk < p.chunks; ++it) {
     tw4_table(chunk);
+    int64_t next = p.chunks;
+    bool has_next = false;
 
     // ---------------- writer stages: wait MMA s, epilogue s, issue MMA s+1
     auto writer = [&](auto sc) {
@@ -718,6 +753,9 @@ __global__ void __launch_bounds__(128, MINB)
       }
     };
     if constexpr (S >= 2) writer(std::integral_constant<int, 0>{});
+    // the next chunk id (written by thread 0 before the barrier just passed)
+    next = s_q[(it + 1) & 3];
+    has_next = next < p.chunks;
     if constexpr (S >= 3) writer(std::integral_constant<int, 1>{});
 
     // ---------------- overlap: gather the next chunk while the last MMAs run
@@ -769,16 +807,38 @@ __global__ void __launch_bounds__(128, MINB)
         // next chunk: its staging buffer is free (gathered above): prefetch the
         // one after, start its stage-1 MMAs, then release the epilogue warps
         // once the store just issued has finished reading s_a
-        if (next + gridDim.x < p.chunks) issue_load(&tm_in, p.in, p.T, next + gridDim.x, s_in, &bars[0]);
+        const int64_t n2 = next_chunk(next);
+        s_q[(it + 2) & 3] = n2;
+        if (n2 < p.chunks) issue_load(&tm_in, p.in, p.T, n2, s_in, &bars[0]);
+        else if (p.pdl == 1 && !triggered) griddep_launch_dependents();
         issue_stage_mma<C, 0>(s_a_u, s_b_u, tD, tA);
         mma_commit(&bars[1]);
         bulk_wait_read0();
         mbar_arrive(&bars[1]);
       }
     }
+    chunk = next;
   }
   }  // PIPE
-  if (tid == 0) bulk_wait0();
+  if (tid == 0) {
+    bulk_wait0();
+    if (p.ctr) {
+      __threadfence();
+      if (atomicAdd(p.ctr + 1, 1ull) == gridDim.x - 1) {  // last CTA out: reset for the next launch
+        p.ctr[0] = 0;
+        p.ctr[1] = 0;
+        __threadfence();
+      }
+    }
+  }
+#ifdef TCFFT_TRACE
+  if (p.trace && tid == 0) {
+    p.trace[blockIdx.x * 4 + 2] = globaltimer_ns();
+    uint32_t sm;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+    p.trace[blockIdx.x * 4 + 3] = sm;
+  }
+#endif
   tc_fence_before();
   __syncthreads();
   tc_fence_after();

@@ -470,6 +470,13 @@ bool build_pass(PassPlan& p, int kind, int N, int64_t count, int64_t images, int
   int by_tmem = 512 / tcols;
   int by_smem = 233472 / (p.smem_bytes + 1024);  // 228 KB per SM incl. 1 KB driver reserve per CTA
   p.ctas_per_sm = std::max(1, std::min(by_tmem, std::min(by_smem, 4)));
+  // Pin occupancy: pad the shared-memory request so that no (ctas_per_sm+1)-th
+  // CTA fits on an SM.  Otherwise an extra CTA (e.g. of the next grid under
+  // programmatic dependent launch) lands beside ctas_per_sm TMEM holders and
+  // spins in tcgen05.alloc, and its statically assigned chunks wait for a
+  // whole neighbour's share: measured 1.8x slower four-step (round 1).
+  const int pinned = ((233472 / (p.ctas_per_sm + 1) - 1024 + 1) + 127) & ~127;
+  if (p.smem_bytes < pinned && p.ctas_per_sm * (pinned + 1024) <= 233472) p.smem_bytes = pinned;
   return true;
 }
 

@@ -19,6 +19,17 @@ DEVI void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
 }
 DEVI void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+// programmatic dependent launch: block until the preceding grid on the stream
+// has completed and its memory is visible (no-op without the launch attribute)
+DEVI unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+DEVI void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// allow the next grid on the stream to start launching (its CTAs take SM slots
+// as ours retire, run their prologue, then griddep_wait)
+DEVI void griddep_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 DEVI void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                : "memory");

@@ -30,10 +30,32 @@ struct KernelEntry {
   void (*launch)(dim3, int, cudaStream_t, const CUtensorMap&, const CUtensorMap&, const KParams&);
 };
 
+// Programmatic dependent launch (default on, TCFFT_PDL=0 disables): a pass
+// kernel may start launching while the previous kernel on the stream retires;
+// its CTAs stage their constants and wait (griddepcontrol.wait) before the
+// first TMA touches the data, so stream order is preserved.
+static int pdl_mode() {
+  static const int m = [] {
+    const char* e = std::getenv("TCFFT_PDL");
+    return e ? std::atoi(e) : 1;
+  }();
+  return m;
+}
+
 template <int E, int R1, int R2, int R3, int MINB, int MODE, bool TW4>
 void launch_tpl(dim3 grid, int smem, cudaStream_t st, const CUtensorMap& a, const CUtensorMap& b,
                 const KParams& p) {
-  tcfft::fft_pass_kernel<E, R1, R2, R3, MINB, MODE, TW4><<<grid, 128, smem, st>>>(a, b, p);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(128);
+  cfg.dynamicSmemBytes = (size_t)smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = p.pdl ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, tcfft::fft_pass_kernel<E, R1, R2, R3, MINB, MODE, TW4>, a, b, p);
 }
 
 #define KENTRY(E, R1, R2, R3, MB, MODE, TW)                                                               \
@@ -316,7 +338,7 @@ void build_fused(tcfftPlanImpl* h, const cudaDeviceProp& prop) {
   f.next_item = F.dynamic ? reinterpret_cast<unsigned long long*>(
                                 reinterpret_cast<char*>(F.counters) + ((objs * sizeof(int32_t) + 7) & ~size_t(7)))
                           : nullptr;
-  cudaFuncSetAttribute(k->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(k->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)prop.sharedMemPerBlockOptin);
   F.grid = (int)std::min<int64_t>(f.items, (int64_t)prop.multiProcessorCount * ctas);
 }
 
@@ -355,7 +377,7 @@ tcfftResult create(tcfftHandle* out, int dims, int nx, int ny, int batch) {
     size_t bb = (p.bblob.size() * 2 + 255) & ~size_t(255);
     size_t tb = (p.tblob.size() * 4 + 255) & ~size_t(255);
     size_t rb_al = (rb + 255) & ~size_t(255);
-    if (cudaMalloc(&d.tables, rb_al + bb + tb + 256) != cudaSuccess) {
+    if (cudaMalloc(&d.tables, rb_al + bb + tb + 512) != cudaSuccess) {
       cudaGetLastError();
       for (auto& q : h->dev) cudaFree(q.tables);
       delete h;
@@ -391,9 +413,34 @@ tcfftResult create(tcfftHandle* out, int dims, int nx, int ny, int batch) {
     // write 16-byte runs whose L2 merging is timing sensitive: keep them lockstep
     k.gather_ahead = (p.tw4_total || p.kind == tcfft::kPassRowT) ? 0 : 1;
     if (const char* e = std::getenv("TCFFT_GATHER_AHEAD")) k.gather_ahead = std::atoi(e);
-    cudaFuncSetAttribute(d.k->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, p.smem_bytes);
+    // pipelined loop: measured faster for the two-stage radix-32-tail plans
+    // (N = 512, 1024: C4 +6%), neutral or slower elsewhere (round 1)
+    k.pipe = (p.S == 2 && p.st[1].R == 32 && !p.tw4_total && p.kind != tcfft::kPassRowT) ? 1 : 0;
+    k.pdl = pdl_mode();
+    // Dynamic chunk tickets for the four-step passes: with static striding and
+    // PDL their CTA->SM placement skews and the pass runs 1.8x slower (round
+    // 1 traces); elsewhere static striding measured equal (C2) or faster (C1:
+    // the ticket round trip sits on a 6 us kernel's critical path).
+    // TCFFT_DYNAMIC=0/1 forces static/dynamic for every pass.
+    {
+      const char* e = std::getenv("TCFFT_DYNAMIC");
+      const bool dyn = e ? std::atoi(e) != 0 : (p.tw4_total != 0 || p.kind == tcfft::kPassRowT);
+      if (dyn) {
+        k.ctr = reinterpret_cast<unsigned long long*>(base + rb_al + bb + tb + 256);
+        cudaMemset(k.ctr, 0, 2 * sizeof(unsigned long long));
+      }
+    }
+    if (const char* e = std::getenv("TCFFT_PDL_MASK"))
+      if (!((std::atoi(e) >> h->dev.size()) & 1)) k.pdl = 0;
+    if (const char* e = std::getenv("TCFFT_PIPE")) k.pipe = std::atoi(e) && !p.tw4_total && p.kind != tcfft::kPassRowT;
+    // the opt-in maximum: one kernel instance serves plans with different
+    // shared-memory requests, occupancy follows each launch's own request
+    cudaFuncSetAttribute(d.k->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)prop.sharedMemPerBlockOptin);
     int64_t slots = (int64_t)prop.multiProcessorCount * p.ctas_per_sm;
     d.grid = (int)std::min<int64_t>(p.chunks, slots);
+#ifdef TCFFT_TRACE
+    cudaMalloc(reinterpret_cast<void**>(&d.kp.trace), (size_t)d.grid * 4 * sizeof(unsigned long long));
+#endif
     h->dev.push_back(d);
   }
   build_fused(h, prop);
@@ -715,6 +762,19 @@ extern "C" tcfftResult tcfftExecC2CStrided(tcfftHandle plan, const void* idata, 
                                                               batch_stride, 0);
   return cudaGetLastError() == cudaSuccess ? TCFFT_SUCCESS : TCFFT_EXEC_FAILED;
 }
+
+#ifdef TCFFT_TRACE
+// trace builds only: copy pass `i`'s per-CTA stamps (start, after PDL wait,
+// end, smid) of the most recent launch into `host` (grid * 4 u64)
+extern "C" int tcfftDebugTrace(tcfftHandle plan, int i, void* host, size_t n) {
+  if (!plan || i < 0 || i >= (int)plan->dev.size()) return -1;
+  const DevPass& d = plan->dev[i];
+  size_t bytes = std::min(n, (size_t)d.grid * 4 * sizeof(unsigned long long));
+  cudaDeviceSynchronize();
+  cudaMemcpy(host, d.kp.trace, bytes, cudaMemcpyDeviceToHost);
+  return d.grid;
+}
+#endif
 
 tcfftResult tcfftDestroy(tcfftHandle plan) {
   if (!valid(plan)) return TCFFT_INVALID_PLAN;

@@ -21,8 +21,15 @@ timeout 600 python bench.py --impl reference --steps 2 --warmup 0 > $OUT/bench_r
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file $OUT/launches_c2_$TAG.csv \
    python bench.py --config c2 --steps 5 --warmup 3 --no-cpu > /dev/null 2>&1
 for c in c2 c1 c3 c4; do
-  n=2; [ $c == c2 ] && n=1; [ $c == c1 ] && n=1
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:fft_pass -s 6 -c $n -o $OUT/prof_${c}_$TAG -f \
+  # skip the 3 warm-up steps: capture the first timed step's launch(es)
+  n=2; sk=6; [ $c == c2 ] && n=1 && sk=3; [ $c == c1 ] && n=1 && sk=6
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:fft_pass -s $sk -c $n -o $OUT/prof_${c}_$TAG -f \
      python bench.py --config $c --steps 2 --warmup 3 --no-cpu > $OUT/ncu_full_${c}_$TAG.log 2>&1
 done
-ls -la $OUT | tail -30
+# keep the merge-back under gpurun's 64 MiB cap: raw CSV for every capture,
+# the .ncu-rep only for the headline config
+for c in c2 c1 c3 c4; do
+  [ -f $OUT/prof_${c}_$TAG.ncu-rep ] && ncu -i $OUT/prof_${c}_$TAG.ncu-rep --page raw --csv > $OUT/prof_${c}_$TAG.raw.csv 2>/dev/null
+  [ $c != c2 ] && rm -f $OUT/prof_${c}_$TAG.ncu-rep
+done
+du -sh $OUT; ls -la $OUT | tail -30

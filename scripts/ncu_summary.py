@@ -30,7 +30,11 @@ UNIT_SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "usecond": 1,
 
 
 def report(path: Path):
-    out = subprocess.run(["ncu", "-i", str(path), "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    raw = path.with_suffix(".raw.csv")
+    if raw.exists():
+        out = raw.read_text()
+    else:
+        out = subprocess.run(["ncu", "-i", str(path), "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     if len(rows) < 3:
         return []
@@ -66,8 +70,10 @@ def main(tag):
              "| config | kernel | time us | DRAM read MB | DRAM write MB | DRAM % | L1/smem % | smem wavefronts | "
              "ld/st bank conflicts | tensor % | issue % | regs |",
              "|---|---|---|---|---|---|---|---|---|---|---|---|"]
-    for rep in sorted((ROOT / "gpurun_out").glob(f"prof_*_{tag}.ncu-rep")):
-        cfg = rep.name.split("_")[1]
+    g = ROOT / "gpurun_out"
+    cfgs = sorted({q.name.split("_")[1] for q in list(g.glob(f"prof_*_{tag}.ncu-rep")) + list(g.glob(f"prof_*_{tag}.raw.csv"))})
+    for cfg in cfgs:
+        rep = g / f"prof_{cfg}_{tag}.ncu-rep"
         ks = report(rep)
         for d in ks:
             short = d["kernel"].split("(")[0].replace("void ", "")
