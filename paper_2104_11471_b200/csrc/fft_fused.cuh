@@ -406,7 +406,7 @@ __global__ void __launch_bounds__(160, MINB)
       using C = typename PT::C;
       constexpr int S = C::S;
       if constexpr (PT::TW4) {
-        const int64_t base = (ch % p.in.spi) * (int64_t)p.in.C;
+        const int64_t base = ((ch % p.in.spi) * (int64_t)p.in.C) >> p.tw4_shift;
         for (int kk = tid; kk <= p.tw4_nk; kk += 128) {
           const int64_t e = (base * (kk < p.tw4_nk ? kk : p.tw4_s)) % p.tw4_total;
           float sn, cs;

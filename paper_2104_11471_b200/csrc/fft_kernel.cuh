@@ -32,6 +32,7 @@ struct KIo {
   int32_t mode;         // IoMode
   int32_t box_rows, n_sub, sub_bytes, chunk_rows;
   int32_t C, spi;       // box: columns per chunk, chunks per image
+  int32_t isplit;       // box: 4D map, image index = outer * isplit + inner (0: 3D)
   int32_t pitch_bytes;  // pitch mode: staging pitch per transform
   int64_t gstride_bytes;  // pitch mode: global distance between transforms (batch_stride * 4)
   int64_t count;        // pitch mode: transforms in the pass
@@ -49,6 +50,7 @@ struct KParams {
   int32_t bbytes;
   int32_t smem_a, a_stride, smem_b, smem_bar, smem_tw4;
   int64_t tw4_total;  // four-step pass 1: full transform length
+  int32_t tw4_shift;  // exponent uses (column >> tw4_shift) (three-step pass B)
   int32_t tw4_nk;     // number of final-stage k values (N1 / R_S)
   int32_t tw4_s;      // N1 / R_S
   int32_t gather_ahead;  // gather chunk i+1 while chunk i's last MMAs run
@@ -90,7 +92,8 @@ struct Cfg {
   __host__ __device__ static constexpr int BOFF(int s) {
     return s == 0 ? 0 : (BSHARE(s) ? BOFF(s - 1) : BOFF(s - 1) + (BSHARE(s - 1) ? 0 : BSZ(s - 1)));
   }
-  __host__ __device__ static constexpr int HSTEP(int s) { return (128 / R(s)) * SBO(s + 1); }
+  // writer row-block interleave, plan.cpp writer_groups()
+  __host__ __device__ static constexpr int HSTEP(int s) { return (R(s) > 32 ? 4 : 128 / R(s)) * SBO(s + 1); }
   __host__ __device__ static constexpr int IMOFF(int s) { return 16 * R(s + 1); }
   __host__ __device__ static constexpr int tmax(int a, int b) { return a > b ? a : b; }
   static constexpr int TMAX = tmax(T(0), tmax(T(S > 1 ? 1 : 0), T(S - 1)));
@@ -199,9 +202,9 @@ DEVI void gather_to_tmem(uint32_t s_in, int gbase, int gstride, uint32_t swzmask
   } else if constexpr (KC == 16) {
     tmem_st16(taddr, v);
   } else {
-    static_assert(KC == 32, "KC");
-    tmem_st16(taddr, v);
-    tmem_st16(taddr + 16, v + 16);
+    static_assert(KC == 32 || KC == 64, "KC");
+#pragma unroll
+    for (int q = 0; q < KC / 16; ++q) tmem_st16(taddr + 16 * q, v + 16 * q);
   }
 }
 
@@ -331,11 +334,19 @@ DEVI void issue_load(const CUtensorMap* tm, const KIo& io, int T, int64_t chunk,
   } else {
     const int32_t img = (int32_t)(chunk / io.spi), cb = (int32_t)(chunk % io.spi);
     for (int i = 0; i < io.n_sub; ++i) {
-      asm volatile(
-          "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
-          "%4}], [%5];" ::"r"(smem_u32(dst + i * io.sub_bytes)),
-          "l"(tm), "r"(cb * io.C), "r"(i * io.box_rows), "r"(img), "r"(smem_u32(bar))
-          : "memory");
+      if (io.isplit)
+        asm volatile(
+            "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
+            "%4, %5}], [%6];" ::"r"(smem_u32(dst + i * io.sub_bytes)),
+            "l"(tm), "r"(cb * io.C), "r"(i * io.box_rows), "r"(img % io.isplit), "r"(img / io.isplit),
+            "r"(smem_u32(bar))
+            : "memory");
+      else
+        asm volatile(
+            "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
+            "%4}], [%5];" ::"r"(smem_u32(dst + i * io.sub_bytes)),
+            "l"(tm), "r"(cb * io.C), "r"(i * io.box_rows), "r"(img), "r"(smem_u32(bar))
+            : "memory");
     }
   }
 }
@@ -355,10 +366,17 @@ DEVI void issue_store(const CUtensorMap* tm, const KIo& io, int T, int64_t chunk
   } else {
     const int32_t img = (int32_t)(chunk / io.spi), cb = (int32_t)(chunk % io.spi);
     for (int i = 0; i < io.n_sub; ++i) {
-      asm volatile(
-          "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(tm),
-          "r"(cb * io.C), "r"(i * io.box_rows), "r"(img), "r"(smem_u32(src + i * io.sub_bytes))
-          : "memory");
+      if (io.isplit)
+        asm volatile(
+            "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4}], [%5];" ::"l"(tm),
+            "r"(cb * io.C), "r"(i * io.box_rows), "r"(img % io.isplit), "r"(img / io.isplit),
+            "r"(smem_u32(src + i * io.sub_bytes))
+            : "memory");
+      else
+        asm volatile(
+            "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(tm),
+            "r"(cb * io.C), "r"(i * io.box_rows), "r"(img), "r"(smem_u32(src + i * io.sub_bytes))
+            : "memory");
     }
   }
   bulk_commit();
@@ -397,10 +415,10 @@ __global__ void __launch_bounds__(128, MINB)
   using C = Cfg<E, R1, R2, R3, MODE>;
   constexpr int S = C::S;
   constexpr int TM = C::TMAX;
-  // Four-step passes write 16-byte runs whose merging in L2 is sensitive to
-  // store timing: they keep the simple (lock-step) chunk loop, measured 1.6x
+  // Transposed-row passes write 16-byte runs whose merging in L2 is sensitive
+  // to store timing: they keep the simple (lock-step) chunk loop, measured 1.6x
   // faster for them than the pipelined loop below (round 1).
-  constexpr bool PIPE_OK = !(TW4 || MODE == kModeRowT) && S >= 2;
+  constexpr bool PIPE_OK = MODE != kModeRowT && S >= 2;
   const bool PIPE = PIPE_OK && p.pipe;
   // Chunk schedule: a CTA's first chunk is blockIdx.x; later ones come from a
   // global ticket counter (thread 0, in load order), so CTAs on slower SMs
@@ -532,7 +550,7 @@ __global__ void __launch_bounds__(128, MINB)
     while (chunk < p.chunks) {
       if constexpr (TW4) {
         // four-step twiddle, strip-base part: A[k] = W_Ntot^{base k}, r = W_Ntot^{base s}
-        const int64_t base = (chunk % p.in.spi) * (int64_t)p.in.C;
+        const int64_t base = ((chunk % p.in.spi) * (int64_t)p.in.C) >> p.tw4_shift;
         for (int kk = tid; kk <= p.tw4_nk; kk += 128) {
           const int64_t e = (base * (kk < p.tw4_nk ? kk : p.tw4_s)) % p.tw4_total;
           float sn, cs;
@@ -667,7 +685,7 @@ __global__ void __launch_bounds__(128, MINB)
   auto tw4_table = [&](int64_t ch) {
     if constexpr (TW4) {
       // four-step twiddle, strip-base part: A[k] = W_Ntot^{base k}, r = W_Ntot^{base s}
-      const int64_t base = (ch % p.in.spi) * (int64_t)p.in.C;
+      const int64_t base = ((ch % p.in.spi) * (int64_t)p.in.C) >> p.tw4_shift;
       for (int kk = tid; kk <= p.tw4_nk; kk += 128) {
         const int64_t e = (base * (kk < p.tw4_nk ? kk : p.tw4_s)) % p.tw4_total;
         float sn, cs;

@@ -79,6 +79,24 @@ struct Bf {
 
 }  // namespace
 
+int writer_groups(int R) { return R > 32 ? 4 : kLanes / R; }
+
+static bool strip_quarter_order() {
+  const char* e = std::getenv("TCFFT_STRIP_QUARTER");
+  return !e || std::atoi(e) != 0;
+}
+
+// Strip-in / rows-out output staging pad (words).  0 = dense [column][k]
+// tile written by ONE TMA store per chunk (final stores 2-way conflicted for
+// N <= 128, 4-way for N = 256); a pad of 8 makes them conflict-free but needs
+// one bulk copy per row: measured 23.3 vs 20.6 TFLOP/s for C3 (N = 128,
+// round 1), so dense unless the conflicts get worse than 2-way.
+static int pitch_pad_words_out(int n) {
+  const char* e = std::getenv("TCFFT_STRIPT_PAD");
+  if (e) return std::atoi(e);
+  return n <= 128 ? 0 : 8;
+}
+
 int pitch_pad_words(int n) {
   // chosen with tests/emulator.py's bank model (see test_plan_emulation.py)
   const char* e = std::getenv("TCFFT_PITCH_PAD");
@@ -86,7 +104,20 @@ int pitch_pad_words(int n) {
   return (n >= 64 && n <= 1024) ? 8 : 0;
 }
 
-std::vector<int> choose_radices(int n) {
+std::vector<int> choose_radices(int n, int kind) {
+  // Strided passes (column strips, transposed rows) of 2048 / 4096 use two
+  // stages with a radix-64 first stage: with three stages the final stage's
+  // 8-row groups hold outputs k, k + 16, ... of one butterfly, which in the
+  // 4-column (16 B) strip / 4-row transposed staging all fall into one bank
+  // (8-way conflicted output stores, tests/emulator.py).  With two stages the
+  // final k run is consecutive.  Radix-64 stage 1 reads its A operand from
+  // TMEM, so the larger DFT block costs no extra shared-memory traffic.
+  const char* e = std::getenv("TCFFT_STRIDED_R64");
+  const bool r64 = !e || std::atoi(e) != 0;
+  if (kind != kPassRow && r64) {
+    if (n == 2048) return {64, 32};
+    if (n == 4096) return {64, 64};
+  }
   switch (n) {
     case 2: return {2};
     case 4: return {4};
@@ -148,8 +179,8 @@ static void box_io(IoDesc& io, int64_t images, int rows, int cols, int C) {
 }
 
 bool build_pass(PassPlan& p, int kind, int N, int64_t count, int64_t images, int cols, std::string* err,
-                int64_t tw4_total) {
-  std::vector<int> rad = choose_radices(N);
+                int64_t tw4_total, int tw4_shift) {
+  std::vector<int> rad = choose_radices(N, kind);
   if (rad.empty()) {
     if (err) *err = "no single-pass radix schedule for N=" + std::to_string(N);
     return false;
@@ -159,6 +190,7 @@ bool build_pass(PassPlan& p, int kind, int N, int64_t count, int64_t images, int
   p.N = N;
   p.S = (int)rad.size();
   p.tw4_total = tw4_total;
+  p.tw4_shift = tw4_shift;
   const bool row_in = kind == kPassRow || kind == kPassRowT;
   if (kind == kPassRow) {
     p.E = chunk_elems_for(N);
@@ -211,18 +243,21 @@ bool build_pass(PassPlan& p, int kind, int N, int64_t count, int64_t images, int
   // pitch (per-transform bulk copies) so that the lanes of a warp, which span
   // several short transforms, fall into different shared-memory banks.
   p.pitch_mode = row_in && N >= 64 && N <= 1024;
-  p.pitch = p.pitch_mode ? N + pitch_pad_words(N) : N;  // words
+  // strip-in / rows-out passes may stage their output rows at a padded pitch
+  // (pitch_pad_words_out)
+  p.pitch = p.pitch_mode ? N + pitch_pad_words(N) : (kind == kPassStripT ? N + pitch_pad_words_out(N) : N);  // words
   const int PW = p.pitch;
   auto w_in = [&](int tr, int n) -> int32_t {
     return row_in ? tr * PW + n : (tr / C) * NN * C + n * C + tr % C;
   };
   auto w_out = [&](int tr, int n) -> int32_t {
     if (kind == kPassRow) return tr * PW + n;
+    if (kind == kPassStripT) return tr * PW + n;
     if (kind == kPassRowT) return n * T + tr;
     return (tr / C) * NN * C + n * C + tr % C;
   };
   p.gstride = (N / rad[0]) * (row_in ? 1 : C);
-  p.ostride = (N / rad[S - 1]) * (kind == kPassRow ? 1 : (kind == kPassRowT ? T : C));
+  p.ostride = (N / rad[S - 1]) * (kind == kPassRow || kind == kPassStripT ? 1 : (kind == kPassRowT ? T : C));
 
   // ---- TMA / bulk-copy descriptors
   if (row_in) {
@@ -245,6 +280,16 @@ bool build_pass(PassPlan& p, int kind, int N, int64_t count, int64_t images, int
   }
   if (kind == kPassRowT) {
     box_io(p.out, images, N, p.cols, T);
+  } else if (kind == kPassStripT && PW == N) {
+    flat_io(p.out, images * (int64_t)N * cols, E, true);  // unpadded: one TMA store per chunk
+  } else if (kind == kPassStripT) {
+    // chunk (image, strip) -> C contiguous rows of N at chunk * E, one bulk
+    // copy per row from the padded staging pitch
+    p.out.mode = kIoPitch;
+    p.out.swz = 0;
+    p.out.n_sub = T;
+    p.out.sub_bytes = N * 4;
+    p.out.total = images * (int64_t)N * cols;
   } else {
     p.out = p.in;
   }
@@ -304,8 +349,18 @@ bool build_pass(PassPlan& p, int kind, int N, int64_t count, int64_t images, int
   cur.reserve(E / R1);
   {
     std::vector<std::tuple<int32_t, int, int>> order;
+    // Rows in staging-address order (conflict-free 4-byte gathers).  Strip
+    // passes with 4-column strips instead give each quarter-warp 8 consecutive
+    // butterflies of one column (still 32 distinct banks for the gather, since
+    // a row of the strip is 4 words): the radix-64 writer's 16-byte stores of
+    // a quarter-warp then cover 128 contiguous bytes.
+    const bool quarter = !row_in && C == 4 && strip_quarter_order();
     for (int tr = 0; tr < T; ++tr)
-      for (int blk = 0; blk < N / R1; ++blk) order.emplace_back(w_in(tr, bnat(blk)), tr, blk);
+      for (int blk = 0; blk < N / R1; ++blk) {
+        const int n = bnat(blk);
+        const int32_t key = quarter ? (((n / 8) * C + tr) * 8 + n % 8) : w_in(tr, n);
+        order.emplace_back(key, tr, blk);
+      }
     std::sort(order.begin(), order.end());
     for (auto& o : order) cur.push_back(Bf{std::get<1>(o), 0, std::get<2>(o)});
   }
@@ -314,7 +369,13 @@ bool build_pass(PassPlan& p, int kind, int N, int64_t count, int64_t images, int
   for (int s = 0; s + 1 < S; ++s) {
     StageInfo& st = p.st[s];
     StageInfo& nx_ = p.st[s + 1];
-    const int R = st.R, Rn = nx_.R, G = kLanes / R;
+    // G = groups of R next-stage rows interleaved block-wise (8-row blocks:
+    // block h of group g at row block (g / G) * G * R/8 + g % G + G * h).  At
+    // least 4, so that a warp's 32 rows come from 4 different groups (radix-64
+    // writers otherwise put 2 groups x 16 consecutive outputs in a warp: 2-way
+    // conflicted strided output stores).  The A region is linear in the row
+    // block (tile_bytes == 16 * sbo), so a super-block may span tiles.
+    const int R = st.R, Rn = nx_.R, G = writer_groups(R);
     const int n2n = st.n2 * R;  // n2 of the next stage
     std::map<std::tuple<int, int, int>, int> gid;
     std::vector<Bf> nxt(E / Rn);
@@ -330,14 +391,14 @@ bool build_pass(PassPlan& p, int kind, int N, int64_t count, int64_t images, int
         g = (int)gid.size();
         gid.emplace(key, g);
         for (int j = 0; j < R; ++j) {
-          int idx = (g / G) * kLanes + ((g % G) + G * (j / 8)) * 8 + j % 8;
+          int idx = (g / G) * G * R + ((g % G) + G * (j / 8)) * 8 + j % 8;
           nxt[idx] = Bf{w.tr, w.k + st.n2 * j, blkn};
         }
       } else {
         g = it->second;
       }
       RowInfo& r = rec(s, (int)rho);
-      r.addr = (g / G) * nx_.tile_bytes + (g % G) * nx_.sbo + mp * 16;
+      r.addr = ((g / G) * G * (R / 8) + (g % G)) * nx_.sbo + mp * 16;
       r.mp = mp;
       r.tw = s > 0 ? 1 : 0;
       double cr, ci, wr, wi;
@@ -357,10 +418,13 @@ bool build_pass(PassPlan& p, int kind, int N, int64_t count, int64_t images, int
       // four-step twiddle W_Ntot^{n2 k1}, n2 = strip base + tr, k1 = k + (N/R_S) j:
       // host part W^{tr k} * (W^{tr s})^j, s = N/R_S; the strip-base part is
       // rebuilt per chunk on the device (kernel tw4 tables).
+      // With tw4_shift (three-step pass B) the exponent is (column >> shift) * k1
+      // and a chunk's C <= 2^shift columns share it: the host part is 1.
       const int64_t s_ = N / rad[S - 1];
+      const int64_t trx = tw4_shift ? 0 : cur[i].tr;
       double cr, ci, wr, wi;
-      root((int64_t)cur[i].tr * cur[i].k, tw4_total, &cr, &ci);
-      root((int64_t)cur[i].tr * s_, tw4_total, &wr, &wi);
+      root(trx * cur[i].k, tw4_total, &cr, &ci);
+      root(trx * s_, tw4_total, &wr, &wi);
       r.mp = cur[i].k;
       r.cr = (float)cr;
       r.ci = (float)ci;
@@ -416,7 +480,8 @@ bool build_pass(PassPlan& p, int kind, int N, int64_t count, int64_t images, int
   p.tblob.clear();  // twiddles come from the per-row (c, w) recurrence
 
   // ---- shared memory / TMEM budget ---------------------------------------
-  const int stage_bytes = row_in ? T * PW * 4 : E * 4;
+  const int stage_bytes = row_in ? T * PW * 4 : E * 4;                            // input staging
+  const int out_bytes = (row_in || kind == kPassStripT) ? T * PW * 4 : E * 4;     // output staging (A buffer)
   {
     int acols = p.st[0].tiles * (p.st[0].KP / 2), dcols = 0;
     for (int s2 = 0; s2 < S; ++s2) dcols = std::max(dcols, p.st[s2].tiles * p.st[s2].NP);
@@ -425,7 +490,7 @@ bool build_pass(PassPlan& p, int kind, int N, int64_t count, int64_t images, int
     p.tmem_cols_needed = tc;
   }
   const int tw4_bytes = tw4_total ? ((N / rad[S - 1]) * 8 + 16 + 127) & ~127 : 0;
-  int a_bytes = stage_bytes;
+  int a_bytes = std::max(stage_bytes, out_bytes);
   for (int s = 1; s < S; ++s) a_bytes = std::max(a_bytes, p.st[s].tiles * p.st[s].tile_bytes);
   a_bytes = (a_bytes + 1023) & ~1023;
   p.a_bytes = a_bytes;
@@ -480,6 +545,47 @@ bool build_pass(PassPlan& p, int kind, int N, int64_t count, int64_t images, int
   return true;
 }
 
+// Three-step 1D transform, N = N1 N2 N3 (each <= 256), n = N2 N3 n1 + N3 n2 + n3,
+// k = k1 + N1 k2 + N1 N2 k3:
+//   pass A: length-N1 FFTs over n1 (column strips of the [N1][N2 N3] input),
+//           twiddle W_N^{(N3 n2 + n3) k1}, each column written as a contiguous
+//           row: Y1[n2][n3][k1]
+//   pass B: length-N2 FFTs over n2 (column strips of [N2][N3 N1], in place),
+//           twiddle W_{N2 N3}^{n3 k2}: Y2[k2][n3][k1]
+//   pass C: length-N3 FFTs over n3 (column strips of each [N3][N1] image k2),
+//           stored straight into natural order X[k3][k2][k1] (4D tensor map)
+// Every strided side moves C * 4 >= 64-byte runs per row: TMA strip copies with
+// 16-byte runs reach ~60% of HBM bandwidth, 64-byte runs ~95%
+// (tests/native/strip_io_probe.cu, round 1), so three passes of full-width
+// traffic beat two passes of 16-byte runs (N1 = N2 = 2048) at these sizes.
+static int build_three_step(Plan& plan, int nx, int lg, int64_t batch, std::string* err) {
+  const int a = lg / 3, b = (lg - a) / 2, c = lg - a - b;
+  const int N1 = 1 << a, N2 = 1 << b, N3 = 1 << c;
+  PassPlan pa, pb, pc;
+  if (!build_pass(pa, kPassStripT, N1, 0, batch, N2 * N3, err, nx)) return 6;
+  if (!build_pass(pb, kPassStrip, N2, 0, batch, N3 * N1, err, (int64_t)N2 * N3, a)) return 6;
+  if (!build_pass(pc, kPassStrip, N3, 0, batch * N2, N1, err)) return 6;
+  if (pb.C > N1 || pc.C > N1 || pb.IMG != 1 || pc.IMG != 1) {
+    if (err) *err = "unsupported three-step geometry";
+    return 6;
+  }
+  // pass C output: X[b][k3][k2][k1] = 4D view {k1, k3 (stride N1 N2), k2 (stride N1), b (stride N)}
+  pc.out.row_stride = (int64_t)N1 * N2;
+  pc.out.img_split = N2;
+  pc.out.img_stride = N1;
+  pc.out.img_stride2 = nx;
+  pa.ws_out = 1;
+  pb.ws_in = pb.ws_out = 1;
+  pc.ws_in = 1;
+  plan.groups = 1;
+  plan.group_bytes = (size_t)batch * (size_t)nx * 4;
+  plan.ws_bytes = plan.group_bytes;
+  plan.passes.push_back(std::move(pa));
+  plan.passes.push_back(std::move(pb));
+  plan.passes.push_back(std::move(pc));
+  return 0;
+}
+
 int build_plan(Plan& plan, int dims, int nx, int ny, int64_t batch, std::string* err) {
   plan = Plan();
   plan.dims = dims;
@@ -512,6 +618,10 @@ int build_plan(Plan& plan, int dims, int nx, int ny, int64_t batch, std::string*
       if (err) *err = "1D sizes above 2^24 are not supported";
       return 6;
     }
+    // Three passes for N >= 2^19 (every strided access keeps >= 64-byte
+    // runs, see below); two passes up to 2^18, whose strips are >= 32 B wide.
+    const char* e3 = std::getenv("TCFFT_THREE_PASS");
+    if (lg >= 19 && (!e3 || std::atoi(e3) != 0)) return build_three_step(plan, nx, lg, batch, err);
     const int N1 = 1 << (lg / 2), N2 = 1 << (lg - lg / 2);
     // The batch is walked in L2-sized groups of G transforms (two launches per
     // group): the group's workspace (reused by every group) stays resident in

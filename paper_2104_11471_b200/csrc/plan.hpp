@@ -22,6 +22,7 @@ enum PassKind : int32_t {
   kPassRow = 0,    // contiguous transforms: element n of transform tr at tr*N + n
   kPassStrip = 1,  // column strip: element n of column tr at n*C + tr (2D column / four-step pass 1)
   kPassRowT = 2,   // contiguous rows in, transposed columns out (four-step pass 2)
+  kPassStripT = 3, // column strip in, each column written as a contiguous row (three-step pass A)
 };
 
 enum IoMode : int32_t {
@@ -40,6 +41,11 @@ struct IoDesc {
   int64_t images = 0;
   int32_t rows = 0, cols = 0;
   int64_t total = 0;
+  // box mode, optional explicit strides (elements; 0 = dense images x rows x cols)
+  // and a split image index img = outer * img_split + inner (4D tensor map:
+  // inner stride img_stride, outer stride img_stride2)
+  int64_t row_stride = 0, img_stride = 0, img_stride2 = 0;
+  int32_t img_split = 0;
 };
 
 struct StageInfo {
@@ -88,6 +94,7 @@ struct PassPlan {
   int32_t pitch_mode, pitch;  // row inputs, 64 <= N <= 1024: padded per-transform staging (words)
   IoDesc in, out;
   int64_t tw4_total;   // four-step pass 1: N of the full transform (extra twiddle), else 0
+  int32_t tw4_shift;   // twiddle exponent uses (column >> tw4_shift) (three-step pass B), else 0
   int32_t ws_in, ws_out;  // pass reads / writes the plan workspace
   int32_t smem_tw4;
   int64_t total;
@@ -116,13 +123,15 @@ struct Plan {
 };
 
 // Radix list chosen for a single-pass transform of length n (product == n).
-std::vector<int> choose_radices(int n);
+std::vector<int> choose_radices(int n, int kind = kPassRow);
+// row-block interleave of a writer stage of radix R (kernel Cfg::HSTEP mirrors it)
+int writer_groups(int R);
 int chunk_elems_for(int n);
 int pitch_pad_words(int n);
 
 // Builds a pass.  kind/geometry as in PassPlan; returns false on unsupported size.
 bool build_pass(PassPlan& p, int kind, int N, int64_t count, int64_t images, int cols, std::string* err,
-                int64_t tw4_total = 0);
+                int64_t tw4_total = 0, int tw4_shift = 0);
 // Builds the whole plan (host-only, no CUDA calls).
 int build_plan(Plan& plan, int dims, int nx, int ny, int64_t batch, std::string* err);
 

@@ -83,12 +83,19 @@ const KernelEntry kKernels[] = {
     KFOUR(4096, 16, 8, 0, 4),     KFOUR(4096, 16, 16, 0, 4),    KFOUR(4096, 16, 32, 0, 4),
     KFOUR(4096, 32, 32, 0, 4),    KFOUR(8192, 16, 16, 8, 2),    KFOUR(16384, 16, 16, 16, 1),
     KFOUR(16384, 16, 16, 8, 1),
+    // strided passes of 2048 / 4096 with a radix-64 first stage (plan.cpp choose_radices)
+    KSTRIP(8192, 64, 32, 0, 2),   KSTRIP(16384, 64, 64, 0, 1),  KFOUR(8192, 64, 32, 0, 2),
+    KFOUR(16384, 64, 64, 0, 1),
+    // three-step passes A / B (strip + twiddle) of length 64
+    KENTRY(4096, 8, 8, 0, 4, 1, true),
 };
 
 const KernelEntry* find_kernel(const PassPlan& p) {
   int r[3] = {0, 0, 0};
   for (int s = 0; s < p.S; ++s) r[s] = p.st[s].R;
-  const int mode = p.kind;  // kPassRow 0, kPassStrip 1, kPassRowT 2 == kernel modes
+  // kPassRow 0, kPassStrip 1, kPassRowT 2 == kernel modes; strip-in / rows-out
+  // passes run the strip kernel (their output addressing is all runtime)
+  const int mode = p.kind == tcfft::kPassStripT ? (int)tcfft::kPassStrip : p.kind;
   const int tw4 = p.tw4_total ? 1 : 0;
   for (const auto& k : kKernels)
     if (k.E == p.E && k.R1 == r[0] && k.R2 == r[1] && k.R3 == r[2] && k.mode == mode && k.tw4 == tw4) return &k;
@@ -224,16 +231,21 @@ tcfftResult make_tmap(CUtensorMap* tm, const tcfft::IoDesc& io, const void* base
             CU_TENSOR_MAP_INTERLEAVE_NONE, io.W == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   } else {
-    cuuint64_t dims[3] = {(cuuint64_t)io.cols, (cuuint64_t)io.rows, (cuuint64_t)io.images};
-    cuuint64_t strides[2] = {(cuuint64_t)io.cols * 4, (cuuint64_t)io.cols * io.rows * 4};
-    cuuint32_t box[3] = {(cuuint32_t)io.C, (cuuint32_t)io.box_rows, 1};
-    cuuint32_t es[3] = {1, 1, 1};
+    const int64_t rs = io.row_stride ? io.row_stride : io.cols;
+    const int64_t is = io.img_stride ? io.img_stride : (int64_t)io.cols * io.rows;
+    const int rank = io.img_split ? 4 : 3;
+    cuuint64_t dims[4] = {(cuuint64_t)io.cols, (cuuint64_t)io.rows,
+                          (cuuint64_t)(io.img_split ? io.img_split : io.images),
+                          (cuuint64_t)(io.img_split ? io.images / io.img_split : 1)};
+    cuuint64_t strides[3] = {(cuuint64_t)rs * 4, (cuuint64_t)is * 4, (cuuint64_t)io.img_stride2 * 4};
+    cuuint32_t box[4] = {(cuuint32_t)io.C, (cuuint32_t)io.box_rows, 1, 1};
+    cuuint32_t es[4] = {1, 1, 1, 1};
     const int run = io.C * 4;
     CUtensorMapSwizzle sw = run == 128  ? CU_TENSOR_MAP_SWIZZLE_128B
                             : run == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
                             : run == 32 ? CU_TENSOR_MAP_SWIZZLE_32B
                                         : CU_TENSOR_MAP_SWIZZLE_NONE;
-    r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, const_cast<void*>(base), dims, strides, box, es,
+    r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_UINT32, rank, const_cast<void*>(base), dims, strides, box, es,
             CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   }
   return r == CUDA_SUCCESS ? TCFFT_SUCCESS : TCFFT_EXEC_FAILED;
@@ -249,6 +261,7 @@ tcfft::KIo to_kio(const tcfft::IoDesc& io, const PassPlan& p) {
   k.chunk_rows = io.chunk_rows;
   k.C = io.C;
   k.spi = io.spi;
+  k.isplit = io.img_split;
   k.pitch_bytes = p.pitch * 4;
   k.gstride_bytes = (int64_t)io.sub_bytes;  // contiguous transforms; strided exec overrides
   k.count = p.count;
@@ -407,6 +420,7 @@ tcfftResult create(tcfftHandle* out, int dims, int nx, int ny, int batch) {
     k.smem_bar = p.smem_bar;
     k.smem_tw4 = p.smem_tw4;
     k.tw4_total = p.tw4_total;
+    k.tw4_shift = p.tw4_shift;
     k.tw4_s = p.N / p.st[p.S - 1].R;
     k.tw4_nk = k.tw4_s;
     // gather-ahead shifts when each CTA's stores land; the four-step passes
@@ -432,7 +446,7 @@ tcfftResult create(tcfftHandle* out, int dims, int nx, int ny, int batch) {
     }
     if (const char* e = std::getenv("TCFFT_PDL_MASK"))
       if (!((std::atoi(e) >> h->dev.size()) & 1)) k.pdl = 0;
-    if (const char* e = std::getenv("TCFFT_PIPE")) k.pipe = std::atoi(e) && !p.tw4_total && p.kind != tcfft::kPassRowT;
+    if (const char* e = std::getenv("TCFFT_PIPE")) k.pipe = std::atoi(e) && p.S >= 2 && p.kind != tcfft::kPassRowT;
     // the opt-in maximum: one kernel instance serves plans with different
     // shared-memory requests, occupancy follows each launch's own request
     cudaFuncSetAttribute(d.k->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)prop.sharedMemPerBlockOptin);
@@ -820,14 +834,14 @@ tcfftResult tcfftDescribePlan(int dims, int nx, int ny, int batch, char* json, s
     for (size_t i = 0; i < plan.passes.size(); ++i) {
       const PassPlan& p = plan.passes[i];
       if (i) s += ", ";
-      s += "{\"kind\": \"" + std::string(p.kind == tcfft::kPassRow ? "row" : (p.kind == tcfft::kPassStrip ? "strip" : "rowT")) + "\", \"N\": " +
+      s += "{\"kind\": \"" + std::string(p.kind == tcfft::kPassRow ? "row" : (p.kind == tcfft::kPassStrip ? "strip" : (p.kind == tcfft::kPassStripT ? "stripT" : "rowT"))) + "\", \"N\": " +
            std::to_string(p.N) + ", \"E\": " + std::to_string(p.E) + ", \"T\": " + std::to_string(p.T) +
            ", \"C\": " + std::to_string(p.C) + ", \"IMG\": " + std::to_string(p.IMG) +
            ", \"chunks\": " + std::to_string(p.chunks) + ", \"flat\": " + std::to_string(p.flat) +
            ", \"W\": " + std::to_string(p.in.W) + ", \"pitch\": " + std::to_string(p.pitch) +
            ", \"in_mode\": " + std::to_string(p.in.mode) + ", \"out_mode\": " + std::to_string(p.out.mode) +
            ", \"swz_in\": " + std::to_string(p.swz_in) + ", \"swz_out\": " + std::to_string(p.swz_out) +
-           ", \"tw4_total\": " + std::to_string(p.tw4_total) + ", \"ws_in\": " + std::to_string(p.ws_in) +
+           ", \"tw4_total\": " + std::to_string(p.tw4_total) + ", \"tw4_shift\": " + std::to_string(p.tw4_shift) + ", \"ws_in\": " + std::to_string(p.ws_in) +
            ", \"ws_out\": " + std::to_string(p.ws_out) + ", \"out_cols\": " + std::to_string(p.cols) + ", \"gstride\": " + std::to_string(p.gstride) +
            ", \"ostride\": " + std::to_string(p.ostride) + ", \"swz\": " + std::to_string(p.swz_in) +
            ", \"smem_bytes\": " + std::to_string(p.smem_bytes) + ", \"smem_a\": " + std::to_string(p.smem_a) +

@@ -133,6 +133,12 @@ def emulate_chunk(pt: PassTables, chunk_words: np.ndarray, stats: dict | None = 
     ophys = _swz(oaddr, swz_out)
     if stats is not None:
         _bank_stats(stats, "final_sts32", ophys, 4)
+    if d["kind"] == "stripT" and d["pitch"] != d["N"]:  # rows at a padded pitch, written back row by row
+        Lo = d["T"] * d["pitch"]
+        obuf = np.zeros(Lo, np.uint32)
+        obuf[ophys // 4] = words
+        assert len(np.unique(ophys)) == ophys.size, "output staging addresses collide"
+        return obuf.reshape(d["T"], d["pitch"])[:, : d["N"]].reshape(-1)
     obuf = np.zeros(L, np.uint32)
     obuf[ophys // 4] = words
     assert len(np.unique(ophys)) == ophys.size, "output staging addresses collide"
@@ -228,3 +234,38 @@ def run_fourstep(n: int, pairs: np.ndarray) -> np.ndarray:
     y = run_pass_strip(p1, pairs.reshape(B, n1, n2, 2))
     z = run_pass_rowT(p2, y.reshape(B * n1, n2, 2), B)
     return z.reshape(B, n, 2)
+
+
+def run_threestep(n: int, pairs: np.ndarray) -> np.ndarray:
+    """Three-pass 1D transform (N >= 2^19) of (B, n, 2) fp16, pass by pass as
+    the planner lays it out (plan.cpp build_three_step)."""
+    B = pairs.shape[0]
+    pa, pb, pc = (PassTables(1, n, 0, B, i) for i in range(3))
+    N1, N2, N3 = pa.d["N"], pb.d["N"], pc.d["N"]
+    shift = pb.d["tw4_shift"]
+    x = np.ascontiguousarray(pairs).view(np.uint32).reshape(B, N1, N2 * N3)
+    # pass A: column strips of [N1][N2 N3], each column -> a contiguous row [col][k1]
+    C = pa.d["C"]
+    y1 = np.empty((B, N2 * N3, N1), np.uint32)
+    for b in range(B):
+        for c0 in range(0, N2 * N3, C):
+            o = emulate_chunk(pa, np.ascontiguousarray(x[b, :, c0: c0 + C]).reshape(-1), tw4_base=c0)
+            y1[b, c0: c0 + C] = o.reshape(C, N1)
+    # pass B: column strips of [N2][N3 N1] in place, twiddle exponent (col >> shift) k2
+    y = y1.reshape(B, N2, N3 * N1)
+    C = pb.d["C"]
+    y2 = np.empty_like(y)
+    for b in range(B):
+        for c0 in range(0, N3 * N1, C):
+            o = emulate_chunk(pb, np.ascontiguousarray(y[b, :, c0: c0 + C]).reshape(-1), tw4_base=c0 >> shift)
+            y2[b, :, c0: c0 + C] = o.reshape(N2, C)
+    # pass C: strips of each [N3][N1] image k2 -> X[b][k3][k2][k1]
+    y = y2.reshape(B, N2, N3, N1)
+    C = pc.d["C"]
+    out = np.empty((B, N3, N2, N1), np.uint32)
+    for b in range(B):
+        for k2 in range(N2):
+            for c0 in range(0, N1, C):
+                o = emulate_chunk(pc, np.ascontiguousarray(y[b, k2, :, c0: c0 + C]).reshape(-1))
+                out[b, :, k2, c0: c0 + C] = o.reshape(N3, C)
+    return out.reshape(B, n)[..., None].view(np.float16).reshape(B, n, 2)

@@ -5,8 +5,10 @@ restatement.  No GPU needed; exercises the real C planner through the C ABI."""
 import numpy as np
 import pytest
 
+from paper_2104_11471_b200 import _lib
+
 from oracle import restate as R
-from tests.emulator import PassTables, run_fourstep, run_pass_row, run_pass_strip
+from tests.emulator import PassTables, emulate_chunk, run_fourstep, run_pass_row, run_pass_strip, run_threestep
 
 SIZES_1D = [2, 4, 8, 16, 32, 64, 128, 256, 512, 1024, 2048, 4096, 8192, 16384]
 
@@ -44,29 +46,46 @@ def test_2d_emulation_matches_fft2(nx, ny, batch):
 
 
 def test_bank_conflicts_report(capsys):
+    """Shared-memory wavefronts per warp instruction of every access pattern,
+    from the planner's real tables.  Strided passes (column strips, four-step)
+    must be conflict-free except the known 2-way cases below."""
     lines = []
-    for dims, nx, ny in [(1, 256, 0), (1, 4096, 0), (1, 512, 0), (1, 1024, 0), (1, 8192, 0), (2, 512, 512)]:
-        for pi in range(2 if dims == 2 else 1):
-            pt = PassTables(dims, nx, ny, 1, pi)
+    for dims, nx, ny in [(1, 256, 0), (1, 4096, 0), (1, 512, 0), (1, 1024, 0), (1, 8192, 0), (2, 512, 512),
+                         (1, 1 << 20, 0), (1, 1 << 22, 0), (1, 1 << 24, 0), (2, 2048, 2048), (2, 4096, 4096)]:
+        for pi in range(len(_lib.describe(dims, nx, ny, 8)["passes"])):
+            pt = PassTables(dims, nx, ny, 8, pi)
+            d = pt.d
             stats = {}
-            if pt.d["kind"] == "row":
-                N = pt.d["N"]
-                x = R.random_pairs([1], pt.d["T"], N)
-                run_pass_row(pt, x, stats)
-            else:
-                x = R.random_pairs([1], 1, nx * ny).reshape(1, nx, ny, 2)
-                run_pass_strip(pt, x, stats)
+            L = d["E"] if d["kind"] in ("strip", "stripT") else d["T"] * d["pitch"]
+            w = np.random.default_rng(pi).integers(0, 2**31, size=L).astype(np.uint32) & 0x3BFF3BFF
+            emulate_chunk(pt, w, stats)
             for k, (tot, cnt, ideal) in stats.items():
-                lines.append(f"{dims}d {nx}x{ny} pass{pi} {k}: {tot / cnt:.2f} wavefronts/instr (ideal {ideal})")
-                assert tot / cnt <= 4 * ideal, (k, tot / cnt)
+                r = tot / cnt / ideal
+                lines.append(f"{dims}d {nx}x{ny} pass{pi} {d['kind']} {k}: {r:.2f}x ideal")
+                # known: N=256 row gather 2-way; strip-in/rows-out final stores 2-way
+                # (dense TMA-stored tile, plan.cpp pitch_pad_words_out)
+                assert r <= (2.0 if d["kind"] in ("row", "stripT") else 1.0), (dims, nx, ny, pi, k, r)
     with capsys.disabled():
         print("\n" + "\n".join(lines))
 
 
-@pytest.mark.parametrize("n,batch", [(1 << 15, 2), (1 << 16, 1), (1 << 17, 1)])
+@pytest.mark.parametrize("n,batch", [(1 << 15, 2), (1 << 16, 1), (1 << 17, 1), (1 << 18, 1)])
 def test_fourstep_emulation_matches_fft(n, batch):
     x = R.random_pairs([11, n], batch, n)
     y = run_fourstep(n, x)
     assert np.isfinite(R.to_complex(y)).all()
     e64 = _errs(y, x, n)
     assert e64 < 1.5e-3, e64
+
+
+@pytest.mark.parametrize("n", [1 << 19, 1 << 22])
+def test_threestep_emulation_matches_fft(n):
+    """1D N >= 2^19: three strided passes (A: strips -> rows + twiddle, B: strips
+    + (col >> shift) twiddle, C: strips -> natural order via a 4D store)."""
+    assert len(_lib.describe(1, n, 0, 1)["passes"]) == 3
+    x = R.random_pairs([13, n], 1, n)
+    y = run_threestep(n, x)
+    assert np.isfinite(R.to_complex(y)).all()
+    e64 = _errs(y, x, n)
+    ref_err = 8.5e-4  # the reference's own rel-L2 vs FP64 at 2^22 (SURVEY.md A3)
+    assert e64 < ref_err, e64
