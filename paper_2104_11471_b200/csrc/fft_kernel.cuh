@@ -65,12 +65,13 @@ namespace dev {
 using namespace sm100;
 
 // ---------------------------------------------------------------- compile-time pass geometry
-enum : int { kModeRow = 0, kModeStrip = 1, kModeRowT = 2 };
+// kModeStrip4: column strips in, 4D tensor-map store out (three-step pass C)
+enum : int { kModeRow = 0, kModeStrip = 1, kModeRowT = 2, kModeStrip4 = 3 };
 
 template <int E_, int R1_, int R2_, int R3_, int MODE_>
 struct Cfg {
   static constexpr int E = E_;
-  static constexpr bool ROW_IN = MODE_ != kModeStrip;   // contiguous rows in (compile-time strides)
+  static constexpr bool ROW_IN = MODE_ == kModeRow || MODE_ == kModeRowT;  // contiguous rows in (compile-time strides)
   static constexpr bool ROW = MODE_ == kModeRow;        // ... and contiguous rows out
   static constexpr int S = (R2_ == 0) ? 1 : ((R3_ == 0) ? 2 : 3);
   static constexpr int N = R1_ * (R2_ ? R2_ : 1) * (R3_ ? R3_ : 1);
@@ -334,14 +335,6 @@ DEVI void issue_load(const CUtensorMap* tm, const KIo& io, int T, int64_t chunk,
   } else {
     const int32_t img = (int32_t)(chunk / io.spi), cb = (int32_t)(chunk % io.spi);
     for (int i = 0; i < io.n_sub; ++i) {
-      if (io.isplit)
-        asm volatile(
-            "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
-            "%4, %5}], [%6];" ::"r"(smem_u32(dst + i * io.sub_bytes)),
-            "l"(tm), "r"(cb * io.C), "r"(i * io.box_rows), "r"(img % io.isplit), "r"(img / io.isplit),
-            "r"(smem_u32(bar))
-            : "memory");
-      else
         asm volatile(
             "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
             "%4}], [%5];" ::"r"(smem_u32(dst + i * io.sub_bytes)),
@@ -351,6 +344,7 @@ DEVI void issue_load(const CUtensorMap* tm, const KIo& io, int T, int64_t chunk,
   }
 }
 
+template <bool D4 = false>
 DEVI void issue_store(const CUtensorMap* tm, const KIo& io, int T, int64_t chunk, const uint8_t* src) {
   if (io.mode == kIoPitch) {
     const int64_t t0 = chunk * T;
@@ -366,7 +360,7 @@ DEVI void issue_store(const CUtensorMap* tm, const KIo& io, int T, int64_t chunk
   } else {
     const int32_t img = (int32_t)(chunk / io.spi), cb = (int32_t)(chunk % io.spi);
     for (int i = 0; i < io.n_sub; ++i) {
-      if (io.isplit)
+      if constexpr (D4)
         asm volatile(
             "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4}], [%5];" ::"l"(tm),
             "r"(cb * io.C), "r"(i * io.box_rows), "r"(img % io.isplit), "r"(img / io.isplit),
@@ -455,7 +449,9 @@ __global__ void __launch_bounds__(128, MINB)
   if (warp == 0) tmem_alloc<C::COLS>(s_tmem);
   if (tid == 0) {
     mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], PIPE ? 2 : 1);  // tcgen05.commit (+ thread 0's arrive when pipelined)
+    // tcgen05.commit (+ thread 0's arrive when pipelined; a second arrival in
+    // the lock-step loop measured 1% slower on C2, round 1)
+    mbar_init(&bars[1], PIPE ? 2 : 1);
     fence_mbar_init();
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_in) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_out) : "memory");
@@ -547,17 +543,11 @@ __global__ void __launch_bounds__(128, MINB)
     uint32_t ld_phase = 0, mma_phase = 0;
     uint8_t* const s_a = smem + p.smem_a;
     const uint32_t s_a_u = smem_u32(s_a);
+    // thread 0 takes chunk tickets one chunk ahead: the (dynamic) ticket's
+    // atomic round trip overlaps a whole chunk instead of delaying the MMAs
+    // (kept in shared memory, s_q[1]: a live register here costs spills)
+    if (tid == 0 && p.ctr) s_q[1] = chunk < p.chunks ? next_chunk(chunk) : p.chunks;
     while (chunk < p.chunks) {
-      if constexpr (TW4) {
-        // four-step twiddle, strip-base part: A[k] = W_Ntot^{base k}, r = W_Ntot^{base s}
-        const int64_t base = ((chunk % p.in.spi) * (int64_t)p.in.C) >> p.tw4_shift;
-        for (int kk = tid; kk <= p.tw4_nk; kk += 128) {
-          const int64_t e = (base * (kk < p.tw4_nk ? kk : p.tw4_s)) % p.tw4_total;
-          float sn, cs;
-          sincospif(-2.0f * (float)e / (float)p.tw4_total, &sn, &cs);
-          s_tw4[kk] = make_float2(cs, sn);
-        }
-      }
       mbar_wait(&bars[0], ld_phase);
       ld_phase ^= 1;
       int g1[C::T(0)];
@@ -576,13 +566,33 @@ __global__ void __launch_bounds__(128, MINB)
       __syncthreads();
       if (tid == 0) {
         tc_fence_after();
-        const int64_t nxt = next_chunk(chunk);
+        const int64_t nxt = p.ctr ? s_q[1] : chunk + gridDim.x;
         s_q[0] = nxt;  // read by all threads after this iteration's last barrier
-        if (nxt < p.chunks) issue_load(&tm_in, p.in, p.T, nxt, s_in, &bars[0]);  // staging buffer is free again
-        else if (p.pdl == 1 && !triggered) griddep_launch_dependents();  // this CTA's last chunk
+        if (nxt < p.chunks) {
+          issue_load(&tm_in, p.in, p.T, nxt, s_in, &bars[0]);  // staging buffer is free again
+          if (p.ctr) s_q[1] = next_chunk(nxt);
+        } else if (p.pdl == 1 && !triggered) {
+          griddep_launch_dependents();  // this CTA's last chunk
+        }
         bulk_wait_read0();  // previous chunk's output store no longer reads s_a
         issue_stage_mma<C, 0>(s_a_u, s_b_u, tD, tA);
         mma_commit(&bars[1]);
+      }
+      if constexpr (TW4) {
+        // four-step twiddle, strip-base part: A[k] = W_Ntot^{base k}, r = W_Ntot^{base s}
+        // (Ntot a power of two).  Computed by warps 1-3 while thread 0 issues the
+        // stage-1 MMAs: the last chunk's final epilogue is done with s_tw4, this
+        // chunk's reads it after the writer barrier(s).
+        if (tid >= 32) {
+          const int64_t base = ((chunk % p.in.spi) * (int64_t)p.in.C) >> p.tw4_shift;
+          for (int kk = tid - 32; kk <= p.tw4_nk; kk += 96) {
+            const int64_t e = (base * (kk < p.tw4_nk ? kk : p.tw4_s)) & (p.tw4_total - 1);
+            float sn, cs;
+            sincospif(-2.0f * (float)e / (float)p.tw4_total, &sn, &cs);
+            s_tw4[kk] = make_float2(cs, sn);
+          }
+        }
+        if constexpr (S == 1) __syncthreads();
       }
       mbar_wait(&bars[1], mma_phase);
       mma_phase ^= 1;
@@ -660,7 +670,7 @@ __global__ void __launch_bounds__(128, MINB)
       fence_proxy_async_smem();
       tc_fence_before();
       __syncthreads();
-      if (tid == 0) issue_store(&tm_out, p.out, p.T, chunk, s_a);
+      if (tid == 0) issue_store<MODE == kModeStrip4>(&tm_out, p.out, p.T, chunk, s_a);
       chunk = s_q[0];
     }
   } else if constexpr (PIPE_OK) {
@@ -820,7 +830,7 @@ __global__ void __launch_bounds__(128, MINB)
     __syncthreads();
     if (tid == 0) {
       tc_fence_after();
-      issue_store(&tm_out, p.out, p.T, chunk, s_a);
+      issue_store<MODE == kModeStrip4>(&tm_out, p.out, p.T, chunk, s_a);
       if (has_next) {
         // next chunk: its staging buffer is free (gathered above): prefetch the
         // one after, start its stage-1 MMAs, then release the epilogue warps

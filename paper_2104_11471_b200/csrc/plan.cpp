@@ -559,7 +559,11 @@ bool build_pass(PassPlan& p, int kind, int N, int64_t count, int64_t images, int
 // (tests/native/strip_io_probe.cu, round 1), so three passes of full-width
 // traffic beat two passes of 16-byte runs (N1 = N2 = 2048) at these sizes.
 static int build_three_step(Plan& plan, int nx, int lg, int64_t batch, std::string* err) {
-  const int a = lg / 3, b = (lg - a) / 2, c = lg - a - b;
+  int a = lg / 3, b = (lg - a) / 2, c = lg - a - b;
+  if (const char* e = std::getenv("TCFFT_THREE_SPLIT")) {  // experiment hook: "a,b,c" (log2 N1, N2, N3)
+    int x, y, z;
+    if (std::sscanf(e, "%d,%d,%d", &x, &y, &z) == 3 && x + y + z == lg) a = x, b = y, c = z;
+  }
   const int N1 = 1 << a, N2 = 1 << b, N3 = 1 << c;
   PassPlan pa, pb, pc;
   if (!build_pass(pa, kPassStripT, N1, 0, batch, N2 * N3, err, nx)) return 6;

@@ -86,8 +86,10 @@ const KernelEntry kKernels[] = {
     // strided passes of 2048 / 4096 with a radix-64 first stage (plan.cpp choose_radices)
     KSTRIP(8192, 64, 32, 0, 2),   KSTRIP(16384, 64, 64, 0, 1),  KFOUR(8192, 64, 32, 0, 2),
     KFOUR(16384, 64, 64, 0, 1),
-    // three-step passes A / B (strip + twiddle) of length 64
-    KENTRY(4096, 8, 8, 0, 4, 1, true),
+    // three-step passes A / B (strip + twiddle) of length 64, pass C (strips in,
+    // 4D natural-order store out) of length 64 .. 256
+    KENTRY(4096, 8, 8, 0, 4, 1, true),  KENTRY(4096, 8, 8, 0, 4, 3, false), KENTRY(4096, 16, 8, 0, 4, 3, false),
+    KENTRY(4096, 16, 16, 0, 4, 3, false),
 };
 
 const KernelEntry* find_kernel(const PassPlan& p) {
@@ -95,7 +97,9 @@ const KernelEntry* find_kernel(const PassPlan& p) {
   for (int s = 0; s < p.S; ++s) r[s] = p.st[s].R;
   // kPassRow 0, kPassStrip 1, kPassRowT 2 == kernel modes; strip-in / rows-out
   // passes run the strip kernel (their output addressing is all runtime)
-  const int mode = p.kind == tcfft::kPassStripT ? (int)tcfft::kPassStrip : p.kind;
+  const int mode = p.kind == tcfft::kPassStripT                          ? (int)tcfft::kPassStrip
+                   : (p.kind == tcfft::kPassStrip && p.out.img_split)  ? 3 /* kModeStrip4 */
+                                                                        : p.kind;
   const int tw4 = p.tw4_total ? 1 : 0;
   for (const auto& k : kKernels)
     if (k.E == p.E && k.R1 == r[0] && k.R2 == r[1] && k.R3 == r[2] && k.mode == mode && k.tw4 == tw4) return &k;
