@@ -214,6 +214,17 @@ bool build_pass(PassPlan& p, int kind, int N, int64_t count, int64_t images, int
     // Column strips of an images x N x cols array: C columns of IMG images per
     // chunk, E = N * C * IMG = max(chunk_elems_for(N), 4 N) (C >= 4: >= 16 B runs).
     p.E = std::max(chunk_elems_for(N), 4 * N);
+    // Plain column strips (2D) of 512 .. 2048 use wider chunks: C = 16 / 8 / 8
+    // columns (64 / 32 / 32-byte runs) instead of 8 / 4 / 4.  Measured with
+    // the lock-step loop: 2D 512^2 0.80 -> 0.88, 1024^2 0.57 -> 0.83 of the
+    // HBM roofline (round 1).  Twiddled (four-step) strips keep 4096.
+    if (kind == kPassStrip && !tw4_total && (N == 512 || N == 1024)) p.E = 8192;
+    if (kind == kPassStrip && !tw4_total && N == 2048) p.E = 16384;
+    {
+      char key[32];  // experiment hook: TCFFT_SCHUNK_<n>=<elems> overrides the strip chunk size
+      std::snprintf(key, sizeof(key), "TCFFT_SCHUNK_%d", N);
+      if (const char* e = std::getenv(key)) p.E = std::atoi(e);
+    }
     int ci = p.E / N;  // C * IMG
     if (ci <= cols) {
       p.C = ci;

@@ -90,6 +90,9 @@ const KernelEntry kKernels[] = {
     // 4D natural-order store out) of length 64 .. 256
     KENTRY(4096, 8, 8, 0, 4, 1, true),  KENTRY(4096, 8, 8, 0, 4, 3, false), KENTRY(4096, 16, 8, 0, 4, 3, false),
     KENTRY(4096, 16, 16, 0, 4, 3, false),
+    // wider 2D column strips (plan.cpp build_pass; 256: TCFFT_SCHUNK_256 experiment)
+    KSTRIP(8192, 16, 32, 0, 2),   KSTRIP(8192, 32, 32, 0, 2),   KSTRIP(16384, 64, 32, 0, 1),
+    KSTRIP(8192, 16, 16, 0, 2),
 };
 
 const KernelEntry* find_kernel(const PassPlan& p) {
@@ -431,9 +434,11 @@ tcfftResult create(tcfftHandle* out, int dims, int nx, int ny, int batch) {
     // write 16-byte runs whose L2 merging is timing sensitive: keep them lockstep
     k.gather_ahead = (p.tw4_total || p.kind == tcfft::kPassRowT) ? 0 : 1;
     if (const char* e = std::getenv("TCFFT_GATHER_AHEAD")) k.gather_ahead = std::atoi(e);
-    // pipelined loop: measured faster for the two-stage radix-32-tail plans
-    // (N = 512, 1024: C4 +6%), neutral or slower elsewhere (round 1)
-    k.pipe = (p.S == 2 && p.st[1].R == 32 && !p.tw4_total && p.kind != tcfft::kPassRowT) ? 1 : 0;
+    // pipelined loop: measured faster only for the N = 1024 (32, 32) row pass
+    // (0.92 vs 0.88 of roofline); slower for the 512 row pass (0.88 vs 0.97),
+    // every column strip (2D 2048^2: 0.48 vs 0.60) and the twiddled passes
+    // (round 1)
+    k.pipe = (p.kind == tcfft::kPassRow && p.S == 2 && p.st[0].R == 32 && p.st[1].R == 32) ? 1 : 0;
     k.pdl = pdl_mode();
     // Dynamic chunk tickets for the four-step passes: with static striding and
     // PDL their CTA->SM placement skews and the pass runs 1.8x slower (round

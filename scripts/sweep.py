@@ -59,7 +59,7 @@ def main():
         for k in (a.sizes or range(8, 25)):
             print(json.dumps(run(1 << k, None, a.reps, peak)), flush=True)
     if a.dims in ("2", "both"):
-        for k in range(8, 13):
+        for k in (a.sizes or range(8, 13)):
             print(json.dumps(run(1 << k, 1 << k, a.reps, peak)), flush=True)
 
 

@@ -62,9 +62,11 @@ def test_bank_conflicts_report(capsys):
             for k, (tot, cnt, ideal) in stats.items():
                 r = tot / cnt / ideal
                 lines.append(f"{dims}d {nx}x{ny} pass{pi} {d['kind']} {k}: {r:.2f}x ideal")
-                # known: N=256 row gather 2-way; strip-in/rows-out final stores 2-way
-                # (dense TMA-stored tile, plan.cpp pitch_pad_words_out)
-                assert r <= (2.0 if d["kind"] in ("row", "stripT") else 1.0), (dims, nx, ny, pi, k, r)
+                # known 2-way: N=256 row gather; strip-in/rows-out final stores (dense
+                # TMA-stored tile, plan.cpp pitch_pad_words_out); the radix-64 writer of
+                # 8-column 2048 strips (either it or the gather conflicts at C = 8)
+                known = d["kind"] in ("row", "stripT") or (d["N"] == 2048 and d["C"] == 8)
+                assert r <= (2.0 if known else 1.0), (dims, nx, ny, pi, k, r)
     with capsys.disabled():
         print("\n" + "\n".join(lines))
 
