@@ -68,6 +68,12 @@ tcfftResult tcfftExecC2CHost(tcfftHandle plan, const void* hin, void* hout);
 tcfftResult tcfftExecC2CStrided(tcfftHandle plan, const void* idata, void* odata, long long stride,
                                 long long batch_stride);
 tcfftResult tcfftDestroy(tcfftHandle plan);
+/* Profiling hook (not part of the reference interface): subsequent
+ * tcfftExecC2C calls launch only the passes whose bit is set in `mask`
+ * (bit i = pass i; ~0u restores normal execution).  Buffer routing is
+ * unchanged, so a partial execution does NOT produce a transform; used by
+ * bench.py to time each pass kernel on its own with CUDA events. */
+tcfftResult tcfftSetPassMask(tcfftHandle plan, unsigned mask);
 
 const char* tcfftGetErrorString(tcfftResult r);
 int tcfftGetVersion(void);

@@ -29,6 +29,7 @@ EXPORTS = (
     "tcfftPlan1D", "tcfftPlan2D", "tcfftSetStream", "tcfftGetWorkspaceSize", "tcfftExecC2C", "tcfftExecC2CHost",
     "tcfftExecC2CStrided",
     "tcfftDestroy", "tcfftGetErrorString", "tcfftGetVersion", "tcfftDescribePlan", "tcfftPlanTables",
+    "tcfftSetPassMask",
 )
 
 
@@ -55,6 +56,7 @@ def load(build_if_missing: bool = True):
     L.tcfftSetStream.argtypes = [vp, vp]
     L.tcfftGetWorkspaceSize.argtypes = [vp, ctypes.POINTER(sz)]
     L.tcfftExecC2C.argtypes = [vp, vp, vp]
+    L.tcfftSetPassMask.argtypes = [vp, ctypes.c_uint]
     if hasattr(L, "tcfftExecC2CStrided"):
         L.tcfftExecC2CStrided.argtypes = [vp, vp, vp, ctypes.c_longlong, ctypes.c_longlong]
     if hasattr(L, "tcfftExecC2CHost"):

@@ -401,8 +401,12 @@ DEVI void issue_stage_mma(uint32_t s_a, uint32_t s_b, uint32_t tD, uint32_t tA) 
 
 }  // namespace dev
 
-template <int E, int R1, int R2, int R3, int MINB, int MODE, bool TW4>
-__global__ void __launch_bounds__(128, MINB)
+// NWG warpgroups of 128 threads: warpgroup w handles tiles t = w, w + NWG, ...
+// of every stage (TMEM lane quarter = warp % 4).  Two warpgroups for the
+// one-CTA-per-SM passes (E = 16384), whose chunk loop is otherwise latency
+// bound on a single warp per SM sub-partition.
+template <int E, int R1, int R2, int R3, int MINB, int MODE, bool TW4, int NWG = 1>
+__global__ void __launch_bounds__(128 * NWG, MINB)
     fft_pass_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ CUtensorMap tm_out,
                     const KParams p) {
   using namespace dev;
@@ -412,7 +416,9 @@ __global__ void __launch_bounds__(128, MINB)
   // Transposed-row passes write 16-byte runs whose merging in L2 is sensitive
   // to store timing: they keep the simple (lock-step) chunk loop, measured 1.6x
   // faster for them than the pipelined loop below (round 1).
-  constexpr bool PIPE_OK = MODE != kModeRowT && S >= 2;
+  constexpr bool PIPE_OK = MODE != kModeRowT && S >= 2 && NWG == 1;
+  constexpr int NT = 128 * NWG;
+  static_assert(C::T(0) % NWG == 0 && C::T(S - 1) % NWG == 0 && C::T(S > 1 ? 1 : 0) % NWG == 0, "NWG tiles");
   const bool PIPE = PIPE_OK && p.pipe;
   // Chunk schedule: a CTA's first chunk is blockIdx.x; later ones come from a
   // global ticket counter (thread 0, in load order), so CTAs on slower SMs
@@ -437,6 +443,8 @@ __global__ void __launch_bounds__(128, MINB)
   uint32_t* s_tmem = reinterpret_cast<uint32_t*>(bars + 2);
   int64_t* s_q = reinterpret_cast<int64_t*>(bars + 4);  // chunk ids in load order (ring of 4)
   const int tid = threadIdx.x, warp = tid >> 5;
+  const int wg = tid >> 7, ltid = tid & 127;  // warpgroup, TMEM lane / MMA row
+  constexpr int TL0 = C::T(0) / NWG;
   const uint32_t s_in_u = smem_u32(s_in), s_b_u = smem_u32(s_b);
 
   // Thread 0 starts the first chunk's TMA load before anything else; the
@@ -465,30 +473,32 @@ __global__ void __launch_bounds__(128, MINB)
     if ((int64_t)blockIdx.x < p.chunks) issue_load(&tm_in, p.in, p.T, (int64_t)blockIdx.x, s_in, &bars[0]);
   }
   // constants: B matrices, once per CTA
-  for (int i = tid; i < p.bbytes / 16; i += 128)
+  for (int i = tid; i < p.bbytes / 16; i += NT)
     reinterpret_cast<uint4*>(s_b)[i] = reinterpret_cast<const uint4*>(p.bblob)[i];
 
   // per-thread row records (host-built, see plan.cpp)
-  auto rec = [&](int s, int t) -> const RowInfo& { return p.rows_tab[((size_t)s * p.tiles_max + t) * 128 + tid]; };
+  auto rec = [&](int s, int t) -> const RowInfo& { return p.rows_tab[((size_t)s * p.tiles_max + t) * 128 + ltid]; };
   // stage-0 writers have c = 1; the final stage needs only its output address
   using RC = Rec<C, TW4>;
-  constexpr bool RT = RC::IN_TMEM;
-  int gb[C::T(0)];
-  int fk[TW4 ? C::T(S - 1) : 1];
-  int waddr[S][TM];
-  float2 wc[S][TM], ww[S][TM];
+  constexpr bool RT = RC::IN_TMEM && NWG == 1;
+  constexpr int TMW = TM / NWG;
+  // this thread's tiles: t = wg + NWG * tt
+  int gb[TL0];
+  int fk[TW4 ? C::T(S - 1) / NWG : 1];
+  int waddr[S][TMW];
+  float2 wc[S][TMW], ww[S][TMW];
 #pragma unroll
-  for (int t = 0; t < C::T(0); ++t) gb[t] = rec(0, t).gbase;
+  for (int tt = 0; tt < TL0; ++tt) gb[tt] = rec(0, wg + NWG * tt).gbase;
 #pragma unroll
   for (int s = 0; s < S; ++s)
 #pragma unroll
-    for (int t = 0; t < TM; ++t) {
-      if (t < C::T(s)) {
-        const RowInfo& r = rec(s, t);
-        waddr[s][t] = r.addr;
-        if (s + 1 < S || TW4) ww[s][t] = make_float2(r.wr, r.wi);
-        if ((s >= 1 && s + 1 < S) || (TW4 && s + 1 == S)) wc[s][t] = make_float2(r.cr, r.ci);
-        if (TW4 && s + 1 == S) fk[t] = r.mp;
+    for (int tt = 0; tt < TMW; ++tt) {
+      if (tt < C::T(s) / NWG) {
+        const RowInfo& r = rec(s, wg + NWG * tt);
+        waddr[s][tt] = r.addr;
+        if (s + 1 < S || TW4) ww[s][tt] = make_float2(r.wr, r.wi);
+        if ((s >= 1 && s + 1 < S) || (TW4 && s + 1 == S)) wc[s][tt] = make_float2(r.cr, r.ci);
+        if (TW4 && s + 1 == S) fk[tt] = r.mp;
       }
     }
 
@@ -497,7 +507,7 @@ __global__ void __launch_bounds__(128, MINB)
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *s_tmem;
-  const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
+  const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
   const uint32_t tD = tbase;
   const uint32_t tA = tbase + (uint32_t)C::DCOLS;
   const uint32_t tR = tbase + (uint32_t)RC::COL + lane_off;  // this lane's row records
@@ -550,17 +560,18 @@ __global__ void __launch_bounds__(128, MINB)
     while (chunk < p.chunks) {
       mbar_wait(&bars[0], ld_phase);
       ld_phase ^= 1;
-      int g1[C::T(0)];
+      int g1[TL0];
       if constexpr (RT) {
         tmem_ld_words<C::T(0)>(tR, reinterpret_cast<uint32_t*>(g1));
         tmem_wait_ld();
       } else {
 #pragma unroll
-        for (int t = 0; t < C::T(0); ++t) g1[t] = gb[t];
+        for (int tt = 0; tt < TL0; ++tt) g1[tt] = gb[tt];
       }
 #pragma unroll
-      for (int t = 0; t < C::T(0); ++t)
-        gather_to_tmem<C>(s_in_u, g1[t], p.gstride, (uint32_t)p.swz_in, tA + lane_off + t * (C::KP(0) / 2));
+      for (int tt = 0; tt < TL0; ++tt)
+        gather_to_tmem<C>(s_in_u, g1[tt], p.gstride, (uint32_t)p.swz_in,
+                          tA + lane_off + (wg + NWG * tt) * (C::KP(0) / 2));
       tmem_wait_st();
       tc_fence_before();
       __syncthreads();
@@ -585,7 +596,7 @@ __global__ void __launch_bounds__(128, MINB)
         // chunk's reads it after the writer barrier(s).
         if (tid >= 32) {
           const int64_t base = ((chunk % p.in.spi) * (int64_t)p.in.C) >> p.tw4_shift;
-          for (int kk = tid - 32; kk <= p.tw4_nk; kk += 96) {
+          for (int kk = tid - 32; kk <= p.tw4_nk; kk += NT - 32) {
             const int64_t e = (base * (kk < p.tw4_nk ? kk : p.tw4_s)) & (p.tw4_total - 1);
             float sn, cs;
             sincospif(-2.0f * (float)e / (float)p.tw4_total, &sn, &cs);
@@ -605,20 +616,20 @@ __global__ void __launch_bounds__(128, MINB)
           tmem_wait_ld();
         }
 #pragma unroll
-        for (int t = 0; t < C::T(s); ++t) {
+        for (int tt = 0; tt < C::T(s) / NWG; ++tt) {
           int ad;
           float2 cc = make_float2(1.f, 0.f), wv;
           if constexpr (RT) {
-            const uint32_t* q = rw + t * RC::WS(s);
+            const uint32_t* q = rw + tt * RC::WS(s);
             ad = (int)q[0];
             wv = make_float2(__uint_as_float(q[1]), __uint_as_float(q[2]));
             if constexpr (s >= 1) cc = make_float2(__uint_as_float(q[3]), __uint_as_float(q[4]));
           } else {
-            ad = waddr[s][t];
-            wv = ww[s][t];
-            if constexpr (s >= 1) cc = wc[s][t];
+            ad = waddr[s][tt];
+            wv = ww[s][tt];
+            if constexpr (s >= 1) cc = wc[s][tt];
           }
-          writer_epilogue<C, s>(tD + lane_off + t * C::NP(s), s_a_u + ad, cc, wv);
+          writer_epilogue<C, s>(tD + lane_off + (wg + NWG * tt) * C::NP(s), s_a_u + ad, cc, wv);
         }
         fence_proxy_async_smem();
         tc_fence_before();
@@ -640,32 +651,32 @@ __global__ void __launch_bounds__(128, MINB)
         tmem_wait_ld();
       }
 #pragma unroll
-      for (int t = 0; t < C::T(S - 1); ++t) {
+      for (int tt = 0; tt < C::T(S - 1) / NWG; ++tt) {
         float2 c4 = make_float2(1.f, 0.f), w4 = make_float2(1.f, 0.f);
         int ad;
         if constexpr (RT)
-          ad = (int)rf[t * RC::FW];
+          ad = (int)rf[tt * RC::FW];
         else
-          ad = waddr[S - 1][t];
+          ad = waddr[S - 1][tt];
         if constexpr (TW4) {
           int kk;
           float2 hc, hw;
           if constexpr (RT) {
-            const uint32_t* q = rf + t * RC::FW;
+            const uint32_t* q = rf + tt * RC::FW;
             kk = (int)q[1];
             hc = make_float2(__uint_as_float(q[2]), __uint_as_float(q[3]));
             hw = make_float2(__uint_as_float(q[4]), __uint_as_float(q[5]));
           } else {
-            kk = fk[t];
-            hc = wc[S - 1][t];
-            hw = ww[S - 1][t];
+            kk = fk[tt];
+            hc = wc[S - 1][tt];
+            hw = ww[S - 1][tt];
           }
           const float2 a = s_tw4[kk], r = s_tw4[p.tw4_nk];
           c4 = make_float2(a.x * hc.x - a.y * hc.y, a.x * hc.y + a.y * hc.x);
           w4 = make_float2(r.x * hw.x - r.y * hw.y, r.x * hw.y + r.y * hw.x);
         }
-        final_epilogue<C, TW4>(tD + lane_off + t * C::NP(S - 1), s_a_u, ad, p.ostride, (uint32_t)p.swz_out, c4,
-                               w4);
+        final_epilogue<C, TW4>(tD + lane_off + (wg + NWG * tt) * C::NP(S - 1), s_a_u, ad, p.ostride,
+                               (uint32_t)p.swz_out, c4, w4);
       }
       fence_proxy_async_smem();
       tc_fence_before();

@@ -551,6 +551,14 @@ bool build_pass(PassPlan& p, int kind, int N, int64_t count, int64_t images, int
   // programmatic dependent launch) lands beside ctas_per_sm TMEM holders and
   // spins in tcgen05.alloc, and its statically assigned chunks wait for a
   // whole neighbour's share: measured 1.8x slower four-step (round 1).
+  // One CTA per SM: two warpgroups split every stage's tiles (kernel NWG)
+  {
+    bool even = true;
+    for (int s2 = 0; s2 < S; ++s2) even = even && (p.st[s2].tiles % 2 == 0);
+    const char* e = std::getenv("TCFFT_NWG");
+    const int want = e ? std::atoi(e) : 2;
+    p.nwg = (p.ctas_per_sm == 1 && even && want >= 2) ? 2 : 1;
+  }
   const int pinned = ((233472 / (p.ctas_per_sm + 1) - 1024 + 1) + 127) & ~127;
   if (p.smem_bytes < pinned && p.ctas_per_sm * (pinned + 1024) <= 233472) p.smem_bytes = pinned;
   return true;

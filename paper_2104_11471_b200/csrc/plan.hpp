@@ -104,6 +104,7 @@ struct PassPlan {
   int32_t tmem_cols; // allocation (power of two >= 32)
   int32_t tmem_a_cols;
   int32_t ctas_per_sm;
+  int32_t nwg = 1;           // warpgroups per CTA (2 for one-CTA-per-SM passes with even tile counts)
   int32_t a_bufs;            // 1 or 2 A / output-staging buffers
   int32_t tmem_cols_needed;
   std::vector<RowInfo> rows_tab;   // [S][tiles_max][128]

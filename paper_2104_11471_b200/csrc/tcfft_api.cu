@@ -25,7 +25,7 @@ namespace {
 using KernelFn = void (*)(CUtensorMap, CUtensorMap, KParams);
 
 struct KernelEntry {
-  int E, R1, R2, R3, mode, tw4;
+  int E, R1, R2, R3, mode, tw4, nwg;
   const void* fn;
   void (*launch)(dim3, int, cudaStream_t, const CUtensorMap&, const CUtensorMap&, const KParams&);
 };
@@ -42,12 +42,12 @@ static int pdl_mode() {
   return m;
 }
 
-template <int E, int R1, int R2, int R3, int MINB, int MODE, bool TW4>
+template <int E, int R1, int R2, int R3, int MINB, int MODE, bool TW4, int NWG>
 void launch_tpl(dim3 grid, int smem, cudaStream_t st, const CUtensorMap& a, const CUtensorMap& b,
                 const KParams& p) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
-  cfg.blockDim = dim3(128);
+  cfg.blockDim = dim3(128 * NWG);
   cfg.dynamicSmemBytes = (size_t)smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
@@ -55,14 +55,15 @@ void launch_tpl(dim3 grid, int smem, cudaStream_t st, const CUtensorMap& a, cons
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = p.pdl ? 1 : 0;
-  cudaLaunchKernelEx(&cfg, tcfft::fft_pass_kernel<E, R1, R2, R3, MINB, MODE, TW4>, a, b, p);
+  cudaLaunchKernelEx(&cfg, tcfft::fft_pass_kernel<E, R1, R2, R3, MINB, MODE, TW4, NWG>, a, b, p);
 }
 
-#define KENTRY(E, R1, R2, R3, MB, MODE, TW)                                                               \
+#define KENTRYW(E, R1, R2, R3, MB, MODE, TW, NWG)                                                         \
   {                                                                                                       \
-    E, R1, R2, R3, MODE, TW, (const void*)&tcfft::fft_pass_kernel<E, R1, R2, R3, MB, MODE, TW>,           \
-        &launch_tpl<E, R1, R2, R3, MB, MODE, TW>                                                          \
+    E, R1, R2, R3, MODE, TW, NWG, (const void*)&tcfft::fft_pass_kernel<E, R1, R2, R3, MB, MODE, TW, NWG>, \
+        &launch_tpl<E, R1, R2, R3, MB, MODE, TW, NWG>                                                     \
   }
+#define KENTRY(E, R1, R2, R3, MB, MODE, TW) KENTRYW(E, R1, R2, R3, MB, MODE, TW, 1)
 #define KROW(E, R1, R2, R3, MB) KENTRY(E, R1, R2, R3, MB, 0, false)
 #define KSTRIP(E, R1, R2, R3, MB) KENTRY(E, R1, R2, R3, MB, 1, false)
 #define KBOTH(E, R1, R2, R3, MB) KROW(E, R1, R2, R3, MB), KSTRIP(E, R1, R2, R3, MB)
@@ -93,6 +94,9 @@ const KernelEntry kKernels[] = {
     // wider 2D column strips (plan.cpp build_pass; 256: TCFFT_SCHUNK_256 experiment)
     KSTRIP(8192, 16, 32, 0, 2),   KSTRIP(8192, 32, 32, 0, 2),   KSTRIP(16384, 64, 32, 0, 1),
     KSTRIP(8192, 16, 16, 0, 2),
+    // one-CTA-per-SM passes with two warpgroups (plan.cpp PassPlan::nwg)
+    KENTRYW(16384, 16, 32, 32, 1, 0, false, 2), KENTRYW(16384, 64, 64, 0, 1, 1, false, 2),
+    KENTRYW(16384, 64, 32, 0, 1, 1, false, 2),
 };
 
 const KernelEntry* find_kernel(const PassPlan& p) {
@@ -104,8 +108,12 @@ const KernelEntry* find_kernel(const PassPlan& p) {
                    : (p.kind == tcfft::kPassStrip && p.out.img_split)  ? 3 /* kModeStrip4 */
                                                                         : p.kind;
   const int tw4 = p.tw4_total ? 1 : 0;
-  for (const auto& k : kKernels)
-    if (k.E == p.E && k.R1 == r[0] && k.R2 == r[1] && k.R3 == r[2] && k.mode == mode && k.tw4 == tw4) return &k;
+  // the planner's warpgroup count if that instantiation exists, else one
+  for (int nwg : {p.nwg, 1})
+    for (const auto& k : kKernels)
+      if (k.E == p.E && k.R1 == r[0] && k.R2 == r[1] && k.R3 == r[2] && k.mode == mode && k.tw4 == tw4 &&
+          k.nwg == nwg)
+        return &k;
   return nullptr;
 }
 
@@ -199,6 +207,7 @@ struct tcfftPlanImpl {
   FusedState fused;
   void* ws = nullptr;
   HostPipe* pipe = nullptr;  // lazily built by tcfftExecC2CHost
+  unsigned pass_mask = ~0u;  // tcfftSetPassMask (profiling)
   void* scratch = nullptr;   // strided views: contiguous staging (lazy)
   size_t scratch_bytes = 0;
   struct GraphEntry {
@@ -508,11 +517,17 @@ tcfftResult tcfftGetWorkspaceSize(tcfftHandle plan, size_t* bytes) {
   return TCFFT_SUCCESS;
 }
 
+tcfftResult tcfftSetPassMask(tcfftHandle plan, unsigned mask) {
+  if (!valid(plan)) return TCFFT_INVALID_PLAN;
+  plan->pass_mask = mask;
+  return TCFFT_SUCCESS;
+}
+
 tcfftResult tcfftExecC2C(tcfftHandle plan, const void* idata, void* odata) {
   if (!valid(plan)) return TCFFT_INVALID_PLAN;
   if (!idata || !odata) return TCFFT_INVALID_VALUE;
   if ((reinterpret_cast<uintptr_t>(idata) | reinterpret_cast<uintptr_t>(odata)) & 15) return TCFFT_INVALID_VALUE;
-  if (plan->fused.k) {
+  if (plan->fused.k && plan->pass_mask == ~0u) {
     const PassPlan& A = plan->plan.passes[0];
     const PassPlan& B = plan->plan.passes[1];
     CUtensorMap a0, a1, b0, b1;
@@ -528,7 +543,7 @@ tcfftResult tcfftExecC2C(tcfftHandle plan, const void* idata, void* odata) {
     plan->fused.k->launch(dim3(plan->fused.grid), plan->fused.smem, plan->stream, a0, a1, b0, b1, f);
     return cudaGetLastError() == cudaSuccess ? TCFFT_SUCCESS : TCFFT_EXEC_FAILED;
   }
-  if (plan->plan.groups > 1) return exec_grouped(plan, idata, odata);
+  if (plan->plan.groups > 1 && plan->pass_mask == ~0u) return exec_grouped(plan, idata, odata);
   return launch_passes(plan, idata, odata, plan->stream);
 }
 
@@ -544,6 +559,10 @@ static tcfftResult launch_passes(tcfftHandle plan, const void* idata, void* odat
     const DevPass& d = plan->dev[i];
     void* dst = p.ws_out ? plan->ws : static_cast<void*>(static_cast<char*>(odata) + goff);
     if (p.ws_in) src = plan->ws;
+    if (!((plan->pass_mask >> i) & 1u)) {
+      src = dst;
+      continue;
+    }
     CUtensorMap tin, tout;
     if (make_tmap(&tin, p.in, src) != TCFFT_SUCCESS || make_tmap(&tout, p.out, dst) != TCFFT_SUCCESS)
       return TCFFT_EXEC_FAILED;
@@ -856,7 +875,7 @@ tcfftResult tcfftDescribePlan(int dims, int nx, int ny, int batch, char* json, s
            ", \"smem_bytes\": " + std::to_string(p.smem_bytes) + ", \"smem_a\": " + std::to_string(p.smem_a) +
            ", \"a_bytes\": " + std::to_string(p.a_bytes) + ", \"tmem_cols\": " + std::to_string(p.tmem_cols) +
            ", \"tmem_a_col\": " + std::to_string(p.tmem_a_cols) +
-           ", \"ctas_per_sm\": " + std::to_string(p.ctas_per_sm) + ", \"a_bufs\": " + std::to_string(p.a_bufs) + ", \"tiles_max\": " +
+           ", \"ctas_per_sm\": " + std::to_string(p.ctas_per_sm) + ", \"nwg\": " + std::to_string(p.nwg) + ", \"a_bufs\": " + std::to_string(p.a_bufs) + ", \"tiles_max\": " +
            std::to_string(p.tiles_max) + ", \"stages\": [";
       for (int sidx = 0; sidx < p.S; ++sidx) {
         const auto& t = p.st[sidx];

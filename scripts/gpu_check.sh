@@ -18,13 +18,16 @@ for c in c2 c1 c3 c4; do
 done
 [ "$MODE" == "quick" ] && exit 0
 timeout 600 python bench.py --impl reference --steps 2 --warmup 0 > $OUT/bench_ref_$TAG.json 2>&1; cat $OUT/bench_ref_$TAG.json
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file $OUT/launches_c2_$TAG.csv \
-   python bench.py --config c2 --steps 5 --warmup 3 --no-cpu > /dev/null 2>&1
+for c in c2 c3 c4; do
+timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:fft_pass --csv \
+   --log-file $OUT/launches_${c}_$TAG.csv python bench.py --config $c --steps 5 --warmup 3 --no-cpu --no-e2e > /dev/null 2>&1
+done
 for c in c2 c1 c3 c4; do
-  # skip the 3 warm-up steps: capture the first timed step's launch(es)
-  n=2; sk=6; [ $c == c2 ] && n=1 && sk=3; [ $c == c1 ] && n=1 && sk=6
+  # skip the warm-up launches: capture every pass of the first timed step
+  # (c1 replays a CUDA graph of 64 launches: 64 pre-capture + 3 x 64 warm-up)
+  case $c in c2) sk=3; n=1;; c1) sk=256; n=1;; c3) sk=9; n=3;; c4) sk=6; n=2;; esac
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:fft_pass -s $sk -c $n -o $OUT/prof_${c}_$TAG -f \
-     python bench.py --config $c --steps 2 --warmup 3 --no-cpu > $OUT/ncu_full_${c}_$TAG.log 2>&1
+     python bench.py --config $c --steps 2 --warmup 3 --no-cpu --no-e2e > $OUT/ncu_full_${c}_$TAG.log 2>&1
 done
 # keep the merge-back under gpurun's 64 MiB cap: raw CSV for every capture,
 # the .ncu-rep only for the headline config
