@@ -551,8 +551,10 @@ __global__ void __launch_bounds__(128 * NWG, MINB)
     // ------------------------------------------------------------ simple loop
     int64_t chunk = blockIdx.x;  // its load was issued in the prologue
     uint32_t ld_phase = 0, mma_phase = 0;
-    uint8_t* const s_a = smem + p.smem_a;
-    const uint32_t s_a_u = smem_u32(s_a);
+    // A operand / output staging: one buffer, or two alternating per chunk
+    // (a_stride != 0: chunk i's writers only wait for chunk i-2's store)
+    uint8_t* s_a = smem + p.smem_a;
+    uint32_t s_a_u = smem_u32(s_a);
     // thread 0 takes chunk tickets one chunk ahead: the (dynamic) ticket's
     // atomic round trip overlaps a whole chunk instead of delaying the MMAs
     // (kept in shared memory, s_q[1]: a live register here costs spills)
@@ -585,7 +587,11 @@ __global__ void __launch_bounds__(128 * NWG, MINB)
         } else if (p.pdl == 1 && !triggered) {
           griddep_launch_dependents();  // this CTA's last chunk
         }
-        bulk_wait_read0();  // previous chunk's output store no longer reads s_a
+        // the output store that last read this chunk's A buffer is done with it
+        if (p.a_stride)
+          bulk_wait_read1();
+        else
+          bulk_wait_read0();
         issue_stage_mma<C, 0>(s_a_u, s_b_u, tD, tA);
         mma_commit(&bars[1]);
       }
@@ -683,6 +689,10 @@ __global__ void __launch_bounds__(128 * NWG, MINB)
       __syncthreads();
       if (tid == 0) issue_store<MODE == kModeStrip4>(&tm_out, p.out, p.T, chunk, s_a);
       chunk = s_q[0];
+      if (p.a_stride) {
+        s_a = (s_a == smem + p.smem_a) ? s_a + p.a_stride : smem + p.smem_a;
+        s_a_u = smem_u32(s_a);
+      }
     }
   } else if constexpr (PIPE_OK) {
   // ---------------------------------------------------------------------

@@ -514,7 +514,7 @@ bool build_pass(PassPlan& p, int kind, int N, int64_t count, int64_t images, int
     const int fixed = p.smem_a + a_bytes + (((int)p.bblob.size() * 2 + 127) & ~127) + tw4_bytes + 64 + 1024;
     const int tmem_ctas = std::max(1, 512 / std::max(32, p.tmem_cols_needed));
 #ifdef TCFFT_PINGPONG
-    p.a_bufs = (fixed + a_bytes) * std::min(tmem_ctas, 4) <= 233472 ? 2 : 1;
+    p.a_bufs = (fixed + a_bytes + 1024) * std::min(tmem_ctas, 4) <= 233472 ? 2 : 1;
 #else
     p.a_bufs = 1;
     (void)fixed;
@@ -551,13 +551,18 @@ bool build_pass(PassPlan& p, int kind, int N, int64_t count, int64_t images, int
   // programmatic dependent launch) lands beside ctas_per_sm TMEM holders and
   // spins in tcgen05.alloc, and its statically assigned chunks wait for a
   // whole neighbour's share: measured 1.8x slower four-step (round 1).
-  // One CTA per SM: two warpgroups split every stage's tiles (kernel NWG)
+  // One CTA per SM: two warpgroups split every stage's tiles (kernel NWG).
+  // TCFFT_NWG=<k> (experiment) asks for k warpgroups wherever tiles divide.
   {
-    bool even = true;
-    for (int s2 = 0; s2 < S; ++s2) even = even && (p.st[s2].tiles % 2 == 0);
     const char* e = std::getenv("TCFFT_NWG");
-    const int want = e ? std::atoi(e) : 2;
-    p.nwg = (p.ctas_per_sm == 1 && even && want >= 2) ? 2 : 1;
+    int want = e ? std::atoi(e) : (p.ctas_per_sm == 1 ? 2 : 1);
+    while (want > 1) {
+      bool div = true;
+      for (int s2 = 0; s2 < S; ++s2) div = div && (p.st[s2].tiles % want == 0);
+      if (div) break;
+      want /= 2;
+    }
+    p.nwg = std::max(1, want);
   }
   const int pinned = ((233472 / (p.ctas_per_sm + 1) - 1024 + 1) + 127) & ~127;
   if (p.smem_bytes < pinned && p.ctas_per_sm * (pinned + 1024) <= 233472) p.smem_bytes = pinned;
