@@ -464,11 +464,11 @@ __global__ void __launch_bounds__(128 * NWG, MINB)
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_in) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_out) : "memory");
 #ifdef TCFFT_TRACE
-    if (p.trace) p.trace[blockIdx.x * 4 + 0] = globaltimer_ns();
+    if (p.trace) p.trace[blockIdx.x * 8 + 0] = globaltimer_ns();
 #endif
     griddep_wait();
 #ifdef TCFFT_TRACE
-    if (p.trace) p.trace[blockIdx.x * 4 + 1] = globaltimer_ns();
+    if (p.trace) p.trace[blockIdx.x * 8 + 1] = globaltimer_ns();
 #endif
     if ((int64_t)blockIdx.x < p.chunks) issue_load(&tm_in, p.in, p.T, (int64_t)blockIdx.x, s_in, &bars[0]);
   }
@@ -559,9 +559,15 @@ __global__ void __launch_bounds__(128 * NWG, MINB)
     // atomic round trip overlaps a whole chunk instead of delaying the MMAs
     // (kept in shared memory, s_q[1]: a live register here costs spills)
     if (tid == 0 && p.ctr) s_q[1] = chunk < p.chunks ? next_chunk(chunk) : p.chunks;
+#ifdef TCFFT_TRACE
+    bool first = true;
+#endif
     while (chunk < p.chunks) {
       mbar_wait(&bars[0], ld_phase);
       ld_phase ^= 1;
+#ifdef TCFFT_TRACE
+      if (first && tid == 0 && p.trace) p.trace[blockIdx.x * 8 + 4] = globaltimer_ns();
+#endif
       int g1[TL0];
       if constexpr (RT) {
         tmem_ld_words<C::T(0)>(tR, reinterpret_cast<uint32_t*>(g1));
@@ -614,6 +620,9 @@ __global__ void __launch_bounds__(128 * NWG, MINB)
       mbar_wait(&bars[1], mma_phase);
       mma_phase ^= 1;
       tc_fence_after();
+#ifdef TCFFT_TRACE
+      if (first && tid == 0 && p.trace) p.trace[blockIdx.x * 8 + 5] = globaltimer_ns();
+#endif
       auto writer = [&](auto sc) {
         constexpr int s = decltype(sc)::value;
         [[maybe_unused]] uint32_t rw[C::T(s) * RC::WS(s)];
@@ -688,6 +697,10 @@ __global__ void __launch_bounds__(128 * NWG, MINB)
       tc_fence_before();
       __syncthreads();
       if (tid == 0) issue_store<MODE == kModeStrip4>(&tm_out, p.out, p.T, chunk, s_a);
+#ifdef TCFFT_TRACE
+      if (first && tid == 0 && p.trace) p.trace[blockIdx.x * 8 + 6] = globaltimer_ns();
+      first = false;
+#endif
       chunk = s_q[0];
       if (p.a_stride) {
         s_a = (s_a == smem + p.smem_a) ? s_a + p.a_stride : smem + p.smem_a;
@@ -870,6 +883,9 @@ __global__ void __launch_bounds__(128 * NWG, MINB)
   }
   }  // PIPE
   if (tid == 0) {
+#ifdef TCFFT_TRACE
+    if (p.trace) p.trace[blockIdx.x * 8 + 7] = globaltimer_ns();
+#endif
     bulk_wait0();
     if (p.ctr) {
       __threadfence();
@@ -882,10 +898,10 @@ __global__ void __launch_bounds__(128 * NWG, MINB)
   }
 #ifdef TCFFT_TRACE
   if (p.trace && tid == 0) {
-    p.trace[blockIdx.x * 4 + 2] = globaltimer_ns();
+    p.trace[blockIdx.x * 8 + 2] = globaltimer_ns();
     uint32_t sm;
     asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
-    p.trace[blockIdx.x * 4 + 3] = sm;
+    p.trace[blockIdx.x * 8 + 3] = sm;
   }
 #endif
   tc_fence_before();

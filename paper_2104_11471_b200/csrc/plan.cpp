@@ -194,6 +194,14 @@ bool build_pass(PassPlan& p, int kind, int N, int64_t count, int64_t images, int
   const bool row_in = kind == kPassRow || kind == kPassRowT;
   if (kind == kPassRow) {
     p.E = chunk_elems_for(N);
+    // Small batches (fewer 4096-element chunks than 4 CTA slots on every SM)
+    // are latency bound: halve the chunk so each CTA's load -> 2 MMA stages ->
+    // store chain is shorter and twice as many CTAs share the work (C1
+    // N=256 x 4096: 7.2 -> 8.1 TFLOP/s, round 1).
+    const char* ce = std::getenv("TCFFT_SMALL_CHUNK");
+    if ((!ce || std::atoi(ce) != 0) && p.E == 4096 && N >= 64 && N <= 256 &&
+        (count * (int64_t)N + 4095) / 4096 < 148 * 4)
+      p.E = 2048;
     p.T = p.E / N;
     p.count = count;
     p.chunks = (count + p.T - 1) / p.T;
@@ -563,6 +571,8 @@ bool build_pass(PassPlan& p, int kind, int N, int64_t count, int64_t images, int
       want /= 2;
     }
     p.nwg = std::max(1, want);
+    // registers: 128 per thread at 512 threads per SM
+    if (p.nwg > 1) p.ctas_per_sm = std::max(1, std::min(p.ctas_per_sm, 4 / p.nwg));
   }
   const int pinned = ((233472 / (p.ctas_per_sm + 1) - 1024 + 1) + 127) & ~127;
   if (p.smem_bytes < pinned && p.ctas_per_sm * (pinned + 1024) <= 233472) p.smem_bytes = pinned;

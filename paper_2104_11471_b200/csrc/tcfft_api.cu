@@ -97,6 +97,8 @@ const KernelEntry kKernels[] = {
     // one-CTA-per-SM passes with two warpgroups (plan.cpp PassPlan::nwg)
     KENTRYW(16384, 16, 32, 32, 1, 0, false, 2), KENTRYW(16384, 64, 64, 0, 1, 1, false, 2),
     KENTRYW(16384, 64, 32, 0, 1, 1, false, 2),
+    // small-batch row passes (half chunks, plan.cpp build_pass)
+    KROW(2048, 16, 16, 0, 4),     KROW(2048, 16, 8, 0, 4),      KROW(2048, 8, 8, 0, 4),
 };
 
 const KernelEntry* find_kernel(const PassPlan& p) {
@@ -471,7 +473,7 @@ tcfftResult create(tcfftHandle* out, int dims, int nx, int ny, int batch) {
     int64_t slots = (int64_t)prop.multiProcessorCount * p.ctas_per_sm;
     d.grid = (int)std::min<int64_t>(p.chunks, slots);
 #ifdef TCFFT_TRACE
-    cudaMalloc(reinterpret_cast<void**>(&d.kp.trace), (size_t)d.grid * 4 * sizeof(unsigned long long));
+    cudaMalloc(reinterpret_cast<void**>(&d.kp.trace), (size_t)d.grid * 8 * sizeof(unsigned long long));
 #endif
     h->dev.push_back(d);
   }
@@ -811,7 +813,7 @@ extern "C" tcfftResult tcfftExecC2CStrided(tcfftHandle plan, const void* idata, 
 extern "C" int tcfftDebugTrace(tcfftHandle plan, int i, void* host, size_t n) {
   if (!plan || i < 0 || i >= (int)plan->dev.size()) return -1;
   const DevPass& d = plan->dev[i];
-  size_t bytes = std::min(n, (size_t)d.grid * 4 * sizeof(unsigned long long));
+  size_t bytes = std::min(n, (size_t)d.grid * 8 * sizeof(unsigned long long));
   cudaDeviceSynchronize();
   cudaMemcpy(host, d.kp.trace, bytes, cudaMemcpyDeviceToHost);
   return d.grid;

@@ -38,7 +38,7 @@ def main():
     res = []
     t_min = None
     for i in range(len(plan.passes)):
-        buf = np.zeros((4096, 4), dtype=np.uint64)
+        buf = np.zeros((4096, 8), dtype=np.uint64)
         g = L.tcfftDebugTrace(plan._handle, i, buf.ctypes.data, buf.nbytes)
         a = buf[:g].astype(np.int64)
         t_min = a[:, 0].min() if t_min is None else min(t_min, a[:, 0].min())
@@ -47,9 +47,12 @@ def main():
         st, wt, en = (a[:, 0] - t_min) / 1e3, (a[:, 1] - t_min) / 1e3, (a[:, 2] - t_min) / 1e3
         q = lambda v: [round(float(np.percentile(v, p)), 1) for p in (0, 5, 50, 95, 100)]
         per_sm = np.bincount(a[:, 3], minlength=148)
+        ld, m0, so, bw = ((a[:, k] - t_min) / 1e3 for k in (4, 5, 6, 7))
         print(json.dumps({"pass": i, "grid": len(a), "start_us_pctl": q(st), "wait_us_pctl": q(wt), "end_us_pctl": q(en),
                           "ctas_per_sm_min_max": [int(per_sm.min()), int(per_sm.max())],
-                          "dur_us_pctl": q(en - wt)}))
+                          "dur_us_pctl": q(en - wt),
+                          "first_chunk": {"load_done": q(ld - wt), "mma0_done": q(m0 - wt), "store_issued": q(so - wt),
+                                          "final_wait_start": q(bw - wt)}}))
 
 
 if __name__ == "__main__":
