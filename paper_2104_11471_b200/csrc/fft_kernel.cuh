@@ -58,6 +58,7 @@ struct KParams {
   int32_t pdl;           // PDL trigger point: 1 = last chunk, 2 = CTA start
   unsigned long long* trace;  // TCFFT_TRACE builds: per-CTA globaltimer stamps
   unsigned long long* ctr;    // dynamic chunk tickets {next, retired CTAs}; null = static
+  int64_t static_chunks;      // with ctr: chunks [0, static_chunks) are statically striped
 };
 
 namespace dev {
@@ -425,8 +426,8 @@ __global__ void __launch_bounds__(128 * NWG, MINB)
   // simply take fewer chunks (static striding left a 15 us tail on C2).  The
   // last CTA to retire resets the counter for the next launch.
   auto next_chunk = [&](int64_t cur) -> int64_t {
-    if (!p.ctr) return cur + gridDim.x;
-    const int64_t c = (int64_t)gridDim.x + (int64_t)atomicAdd(p.ctr, 1ull);
+    if (!p.ctr || cur + gridDim.x < p.static_chunks) return cur + gridDim.x;
+    const int64_t c = p.static_chunks + (int64_t)atomicAdd(p.ctr, 1ull);
     return c < p.chunks ? c : p.chunks;
   };
 

@@ -451,18 +451,25 @@ tcfftResult create(tcfftHandle* out, int dims, int nx, int ny, int batch) {
     // (round 1)
     k.pipe = (p.kind == tcfft::kPassRow && p.S == 2 && p.st[0].R == 32 && p.st[1].R == 32) ? 1 : 0;
     k.pdl = pdl_mode();
-    // Dynamic chunk tickets for the four-step passes: with static striding and
-    // PDL their CTA->SM placement skews and the pass runs 1.8x slower (round
-    // 1 traces); elsewhere static striding measured equal (C2) or faster (C1:
-    // the ticket round trip sits on a 6 us kernel's critical path).
-    // TCFFT_DYNAMIC=0/1 forces static/dynamic for every pass.
-    {
+    // Chunk scheduling (kernel next_chunk): static striding, except that the
+    // last two rounds of chunks are handed out by ticket, fetched one chunk
+    // ahead, so CTAs on slower SMs take fewer of them (the static tail spread
+    // was ~13 us of a 97 us C2 pass).  Measured equal or better everywhere
+    // (four-step 0.80 -> 0.83, C4 +1%), round 1.  Passes with fewer than three
+    // rounds stay static: the ticket + retire atomics cost short kernels (C1).
+    // TCFFT_DYNAMIC=0: static; 1: tickets for every chunk after the first.
+    const int dyn_mode = [] {
       const char* e = std::getenv("TCFFT_DYNAMIC");
-      const bool dyn = e ? std::atoi(e) != 0 : (p.tw4_total != 0 || p.kind == tcfft::kPassRowT);
-      if (dyn) {
-        k.ctr = reinterpret_cast<unsigned long long*>(base + rb_al + bb + tb + 256);
-        cudaMemset(k.ctr, 0, 2 * sizeof(unsigned long long));
-      }
+      return e ? std::atoi(e) : 2;
+    }();
+    const int64_t slots0 = (int64_t)prop.multiProcessorCount * p.ctas_per_sm;
+    const int64_t grid0 = std::min<int64_t>(p.chunks, slots0);
+    // (the pipelined loop takes its tickets on the critical path: static there,
+    // 2D 1024^2 0.80 vs 0.73)
+    const bool dyn = dyn_mode == 1 || (dyn_mode == 2 && p.chunks / grid0 >= 3 && !k.pipe);
+    if (dyn) {
+      k.ctr = reinterpret_cast<unsigned long long*>(base + rb_al + bb + tb + 256);
+      cudaMemset(k.ctr, 0, 2 * sizeof(unsigned long long));
     }
     if (const char* e = std::getenv("TCFFT_PDL_MASK"))
       if (!((std::atoi(e) >> h->dev.size()) & 1)) k.pdl = 0;
@@ -472,6 +479,8 @@ tcfftResult create(tcfftHandle* out, int dims, int nx, int ny, int batch) {
     cudaFuncSetAttribute(d.k->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)prop.sharedMemPerBlockOptin);
     int64_t slots = (int64_t)prop.multiProcessorCount * p.ctas_per_sm;
     d.grid = (int)std::min<int64_t>(p.chunks, slots);
+    k.static_chunks = d.grid;
+    if (k.ctr && dyn_mode == 2) k.static_chunks = std::max<int64_t>(d.grid, (p.chunks / d.grid - 2) * d.grid);
 #ifdef TCFFT_TRACE
     cudaMalloc(reinterpret_cast<void**>(&d.kp.trace), (size_t)d.grid * 8 * sizeof(unsigned long long));
 #endif
