@@ -161,9 +161,17 @@ def run_ours(args, cfg):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # one process per GPU; TCFFT_BENCH_BACKEND=gloo (test hook) lets several
+    # ranks share one GPU to exercise the multi-rank timing path
+    backend = os.environ.get("TCFFT_BENCH_BACKEND", "nccl")
+    if backend != "nccl":
+        local = local % torch.cuda.device_count()
     if world > 1:
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
 
@@ -229,7 +237,7 @@ def run_ours(args, cfg):
     clocks = clk.stop(local)
     ms = e0.elapsed_time(e1) / steps
     if world > 1:
-        t = torch.tensor([ms], device=dev)
+        t = torch.tensor([ms], device=dev if backend == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = t.item()
         dist.barrier()
@@ -280,7 +288,7 @@ def run_ours(args, cfg):
     e2e_ms = e0.elapsed_time(e1) / e2e_steps
     e2e_wall_ms = (time.perf_counter() - t0) * 1e3 / e2e_steps
     if world > 1:
-        t = torch.tensor([e2e_ms], device=dev)
+        t = torch.tensor([e2e_ms], device=dev if backend == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = t.item()
 
