@@ -221,8 +221,9 @@ bool build_pass(PassPlan& p, int kind, int N, int64_t count, int64_t images, int
   } else {
     // Column strips of an images x N x cols array: C columns of IMG images per
     // chunk, E = N * C * IMG = max(chunk_elems_for(N), 4 N) (C >= 4: >= 16 B runs).
-    // (columns of 8192 / 16384 rows: 2- / 1-column strips, the chunk is capped)
-    p.E = std::min(std::max(chunk_elems_for(N), 4 * N), 16384);
+    // (>= 4 columns: TMA boxes move >= 16 bytes per row, so 2D columns of
+    // 8192+ rows would need 128 KB chunks: not supported)
+    p.E = std::max(chunk_elems_for(N), 4 * N);
     // Plain column strips (2D) of 512 .. 2048 use wider chunks: C = 16 / 8 / 8
     // columns (64 / 32 / 32-byte runs) instead of 8 / 4 / 4.  Measured with
     // the lock-step loop: 2D 512^2 0.80 -> 0.88, 1024^2 0.57 -> 0.83 of the

@@ -97,8 +97,6 @@ const KernelEntry kKernels[] = {
     // one-CTA-per-SM passes with two warpgroups (plan.cpp PassPlan::nwg)
     KENTRYW(16384, 16, 32, 32, 1, 0, false, 2), KENTRYW(16384, 64, 64, 0, 1, 1, false, 2),
     KENTRYW(16384, 64, 32, 0, 1, 1, false, 2),
-    // 2D columns of 8192 / 16384 rows (2- / 1-column strips)
-    KENTRYW(16384, 16, 16, 32, 1, 1, false, 2), KENTRYW(16384, 16, 32, 32, 1, 1, false, 2),
     // column strips of 256 columns for N <= 8 (2D nx <= 8 with ny > 256)
     KSTRIP(512, 2, 0, 0, 4),      KSTRIP(1024, 4, 0, 0, 4),     KSTRIP(2048, 8, 0, 0, 4),
     // small-batch row passes (half chunks, plan.cpp build_pass)

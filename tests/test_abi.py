@@ -64,7 +64,8 @@ def test_describe_2d_passes(nx, ny):
 
 @pytest.mark.parametrize("args,code", [((1, 3, 0, 1), INVALID_SIZE), ((1, 0, 0, 1), INVALID_SIZE),
                                        ((1, 1, 0, 1), INVALID_SIZE), ((2, 8, 6, 1), INVALID_SIZE),
-                                       ((1, 256, 0, 0), INVALID_VALUE), ((1, 1 << 25, 0, 1), NOT_SUPPORTED)])
+                                       ((1, 256, 0, 0), INVALID_VALUE), ((1, 1 << 25, 0, 1), NOT_SUPPORTED),
+                                       ((2, 8192, 16, 1), NOT_SUPPORTED)])
 def test_describe_rejects_like_the_reference(args, code):
     st, _ = _describe(*args)
     assert st == code

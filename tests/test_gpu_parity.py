@@ -139,7 +139,8 @@ def test_tone_peaks_at_conjugate_bin():
 
 @pytest.mark.parametrize("nx,ny,batch", [(16, 16, 3), (64, 32, 2), (32, 64, 2), (256, 256, 2), (512, 256, 1),
                                          (512, 512, 2), (1024, 1024, 1), (2048, 64, 1), (4096, 16, 1),
-                                         (8, 256, 2), (2048, 2048, 1), (4096, 512, 1)])
+                                         (8, 256, 2), (2048, 2048, 1), (4096, 512, 1), (8, 1024, 2),
+                                         (2, 4096, 1)])
 def test_2d_parity(nx, ny, batch):
     x = R.random_pairs([33, nx, ny], batch, nx * ny)
     y = _run(x, nx, ny)
