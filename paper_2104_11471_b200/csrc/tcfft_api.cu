@@ -186,8 +186,15 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
+// Ticket counters {next, retired} per launch slot: each launch of a pass takes
+// the next of kTicketSlots slots (the kernel's last CTA resets its slot), so
+// up to kTicketSlots executions of one plan may be in flight concurrently on
+// different streams without sharing a counter.
+constexpr int kTicketSlots = 64;
+
 struct DevPass {
   const KernelEntry* k = nullptr;
+  mutable unsigned launches = 0;  // launch counter (ticket slot), atomically incremented
   void* tables = nullptr;  // rows | bblob | tblob
   KParams kp{};
   int grid = 0;
@@ -410,7 +417,7 @@ tcfftResult create(tcfftHandle* out, int dims, int nx, int ny, int batch) {
     size_t bb = (p.bblob.size() * 2 + 255) & ~size_t(255);
     size_t tb = (p.tblob.size() * 4 + 255) & ~size_t(255);
     size_t rb_al = (rb + 255) & ~size_t(255);
-    if (cudaMalloc(&d.tables, rb_al + bb + tb + 512) != cudaSuccess) {
+    if (cudaMalloc(&d.tables, rb_al + bb + tb + 256 + kTicketSlots * 16) != cudaSuccess) {
       cudaGetLastError();
       for (auto& q : h->dev) cudaFree(q.tables);
       delete h;
@@ -471,7 +478,7 @@ tcfftResult create(tcfftHandle* out, int dims, int nx, int ny, int batch) {
     const bool dyn = dyn_mode == 1 || (dyn_mode == 2 && p.chunks / grid0 >= 3 && !k.pipe);
     if (dyn) {
       k.ctr = reinterpret_cast<unsigned long long*>(base + rb_al + bb + tb + 256);
-      cudaMemset(k.ctr, 0, 2 * sizeof(unsigned long long));
+      cudaMemset(k.ctr, 0, kTicketSlots * 2 * sizeof(unsigned long long));
     }
     if (const char* e = std::getenv("TCFFT_PDL_MASK"))
       if (!((std::atoi(e) >> h->dev.size()) & 1)) k.pdl = 0;
@@ -582,6 +589,7 @@ static tcfftResult launch_passes(tcfftHandle plan, const void* idata, void* odat
     KParams kp = d.kp;
     kp.in.gptr = static_cast<const uint8_t*>(src);
     kp.out.gptr = static_cast<const uint8_t*>(dst);
+    if (kp.ctr) kp.ctr += 2 * (__atomic_fetch_add(&d.launches, 1u, __ATOMIC_RELAXED) % kTicketSlots);
     d.k->launch(dim3(d.grid), p.smem_bytes, st, tin, tout, kp);
     if (cudaGetLastError() != cudaSuccess) return TCFFT_EXEC_FAILED;
     src = dst;
@@ -789,6 +797,7 @@ extern "C" tcfftResult tcfftExecC2CStrided(tcfftHandle plan, const void* idata, 
     kp.in.gptr = static_cast<const uint8_t*>(idata);
     kp.out.gptr = static_cast<const uint8_t*>(odata);
     kp.in.gstride_bytes = kp.out.gstride_bytes = batch_stride * 4;
+    if (kp.ctr) kp.ctr += 2 * (__atomic_fetch_add(&d.launches, 1u, __ATOMIC_RELAXED) % kTicketSlots);
     d.k->launch(dim3(d.grid), p.smem_bytes, plan->stream, t0, t1, kp);
     return cudaGetLastError() == cudaSuccess ? TCFFT_SUCCESS : TCFFT_EXEC_FAILED;
   }

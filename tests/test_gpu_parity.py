@@ -219,3 +219,28 @@ def test_2d_fused_single_launch_matches_two_pass(nx, ny, batch, monkeypatch):
     tc.execute(tc.plan_2d(nx, ny, batch), x, out=y1)
     torch.cuda.synchronize()
     assert torch.equal(y1.view(torch.int16), y2.view(torch.int16))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("nx,ny,batch", [(4096, None, 2048), (512, 512, 64)])
+def test_one_plan_on_two_streams_concurrently(nx, ny, batch):
+    """A plan without a workspace is shareable: executions on different streams
+    may overlap (each launch takes its own chunk-ticket slot).  Bit-exact vs
+    serial execution."""
+    tc = _tc()
+    total = nx * (ny or 1)
+    plan = tc.plan_1d(nx, batch) if ny is None else tc.plan_2d(nx, ny, batch)
+    g = torch.Generator(device="cuda").manual_seed(7)
+    xs = [(torch.rand((batch, total, 2), device="cuda", generator=g) * 2 - 1).half() for _ in range(2)]
+    ref = [torch.empty_like(x) for x in xs]
+    for x, r in zip(xs, ref):
+        tc.execute(plan, x, out=r)
+    torch.cuda.synchronize()
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    outs = [torch.empty_like(x) for x in xs]
+    for _ in range(8):
+        for x, o, s in zip(xs, outs, streams):
+            tc.execute(plan, x, out=o, stream=s)
+    torch.cuda.synchronize()
+    for o, r in zip(outs, ref):
+        assert torch.equal(o.view(torch.int16), r.view(torch.int16))
