@@ -84,9 +84,10 @@ struct Cfg {
   __host__ __device__ static constexpr int SBO(int s) { return 32 * R(s) + 16; }  // padded: consecutive 8-row groups hit distinct banks
   __host__ __device__ static constexpr int TILEB(int s) { return 16 * SBO(s); }
   // B matrices: stage 0 (interleaved K), then one planar-K matrix per distinct
-  // radix run (stages s >= 2 with R(s) == R(s-1) share the previous matrix)
+  // radix run (stages s >= 2 with R(s) == R(s-1) share the previous matrix;
+  // TCFFT_NO_BDEDUPE builds keep one copy per stage)
   __host__ __device__ static constexpr int BSZ(int s) { return KP(s) * NP(s) * 2; }
-#ifndef TCFFT_BDEDUPE
+#ifdef TCFFT_NO_BDEDUPE
   __host__ __device__ static constexpr bool BSHARE(int s) { return false; }
 #else
   __host__ __device__ static constexpr bool BSHARE(int s) { return s >= 2 && R(s) == R(s - 1); }

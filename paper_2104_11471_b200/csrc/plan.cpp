@@ -462,7 +462,7 @@ bool build_pass(PassPlan& p, int kind, int N, int64_t count, int64_t images, int
     StageInfo& st = p.st[s];
     const int R = st.R, KP = st.KP, NP = st.NP;
     st.b_bytes = KP * NP * 2;
-#ifdef TCFFT_BDEDUPE
+#ifndef TCFFT_NO_BDEDUPE
     if (s >= 2 && p.st[s - 1].R == R) {  // identical planar-K matrix: share it
 #else
     if (false) {
