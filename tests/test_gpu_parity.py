@@ -244,3 +244,26 @@ def test_one_plan_on_two_streams_concurrently(nx, ny, batch):
     torch.cuda.synchronize()
     for o, r in zip(outs, ref):
         assert torch.equal(o.view(torch.int16), r.view(torch.int16))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("nx,ny,batch", [(4096, None, 1 << 18), (1 << 22, None, 512), (512, 512, 8192)])
+def test_large_batches_beyond_2gib(nx, ny, batch):
+    """4-8 GiB buffers (int64 chunk math, TMA coordinate ranges): Parseval over
+    the whole batch, and a sampled transform against the oracle."""
+    tc = _tc()
+    total = nx * (ny or 1)
+    g = torch.Generator(device="cuda").manual_seed(99)
+    x = (torch.rand((batch, total, 2), device="cuda", generator=g) * 2 - 1).half()
+    plan = tc.plan_1d(nx, batch) if ny is None else tc.plan_2d(nx, ny, batch)
+    tc.execute(plan, x)  # in place
+    torch.cuda.synchronize()
+    g = torch.Generator(device="cuda").manual_seed(99)
+    x0 = (torch.rand((batch, total, 2), device="cuda", generator=g) * 2 - 1).half()
+    xs = (x0.float() ** 2).sum(dim=(1, 2))
+    ys = (x.float() ** 2).sum(dim=(1, 2))
+    ratio = (ys / (total * xs)).cpu().numpy()
+    assert np.isfinite(ratio).all() and np.abs(ratio - 1).max() < 5e-3
+    last = batch - 1
+    _gates(x[last:].cpu().numpy(), x0[last:].cpu().numpy(), nx, ny)
+    plan.destroy()
