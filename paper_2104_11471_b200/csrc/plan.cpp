@@ -104,7 +104,7 @@ int pitch_pad_words(int n) {
   return (n >= 64 && n <= 1024) ? 8 : 0;
 }
 
-std::vector<int> choose_radices(int n, int kind) {
+std::vector<int> choose_radices(int n, int kind, bool twiddled) {
   // Strided passes (column strips, transposed rows) of 2048 / 4096 use two
   // stages with a radix-64 first stage: with three stages the final stage's
   // 8-row groups hold outputs k, k + 16, ... of one butterfly, which in the
@@ -117,6 +117,16 @@ std::vector<int> choose_radices(int n, int kind) {
   if (kind != kPassRow && r64) {
     if (n == 2048) return {64, 32};
     if (n == 4096) return {64, 64};
+  }
+  // Plain column strips of 512 / 1024 (2D, 8192-element chunks): a radix-64
+  // last stage (fewer, larger MMA tiles, one 64-output epilogue per lane):
+  // C4 +1% (round 1).
+  // TCFFT_STRIP_R64=0 restores [16, 32] / [32, 32].
+  // (2D column strips 1024^2: 0.75 -> 0.83 of roofline)
+  if (kind == kPassStrip && !twiddled && (n == 512 || n == 1024)) {
+    const char* e2 = std::getenv("TCFFT_STRIP_R64");
+    const int v = e2 ? std::atoi(e2) : 1;
+    if (v) return n == 512 ? std::vector<int>{8, 64} : std::vector<int>{16, 64};
   }
   switch (n) {
     case 2: return {2};
@@ -180,7 +190,7 @@ static void box_io(IoDesc& io, int64_t images, int rows, int cols, int C) {
 
 bool build_pass(PassPlan& p, int kind, int N, int64_t count, int64_t images, int cols, std::string* err,
                 int64_t tw4_total, int tw4_shift) {
-  std::vector<int> rad = choose_radices(N, kind);
+  std::vector<int> rad = choose_radices(N, kind, tw4_total != 0);
   if (rad.empty()) {
     if (err) *err = "no single-pass radix schedule for N=" + std::to_string(N);
     return false;

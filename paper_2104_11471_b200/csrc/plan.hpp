@@ -124,7 +124,7 @@ struct Plan {
 };
 
 // Radix list chosen for a single-pass transform of length n (product == n).
-std::vector<int> choose_radices(int n, int kind = kPassRow);
+std::vector<int> choose_radices(int n, int kind = kPassRow, bool twiddled = false);
 // row-block interleave of a writer stage of radix R (kernel Cfg::HSTEP mirrors it)
 int writer_groups(int R);
 int chunk_elems_for(int n);

@@ -93,7 +93,7 @@ const KernelEntry kKernels[] = {
     KENTRY(4096, 16, 16, 0, 4, 3, false),
     // wider 2D column strips (plan.cpp build_pass; 256: TCFFT_SCHUNK_256 experiment)
     KSTRIP(8192, 16, 32, 0, 2),   KSTRIP(8192, 32, 32, 0, 2),   KSTRIP(16384, 64, 32, 0, 1),
-    KSTRIP(8192, 16, 16, 0, 2),
+    KSTRIP(8192, 16, 16, 0, 2),   KSTRIP(8192, 8, 64, 0, 2),    KSTRIP(8192, 16, 64, 0, 2),
     // one-CTA-per-SM passes with two warpgroups (plan.cpp PassPlan::nwg)
     KENTRYW(16384, 16, 32, 32, 1, 0, false, 2), KENTRYW(16384, 64, 64, 0, 1, 1, false, 2),
     KENTRYW(16384, 64, 32, 0, 1, 1, false, 2),
