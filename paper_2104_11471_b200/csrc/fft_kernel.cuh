@@ -78,6 +78,10 @@ struct Cfg {
   static constexpr int N = R1_ * (R2_ ? R2_ : 1) * (R3_ ? R3_ : 1);
   __host__ __device__ static constexpr int R(int s) { return s == 0 ? R1_ : (s == 1 ? R2_ : R3_); }
   static constexpr int RL = R(S - 1);
+  // radix-64 first stages gather their TMEM A operand in planar K order
+  // (re_0..re_63, im_0..im_63) so that their B matrix equals the planar one of
+  // a following radix-64 stage (shared: 32 KB of SMEM saved); plan.cpp mirrors
+  static constexpr bool PLANAR0 = R1_ == 64;
   __host__ __device__ static constexpr int KP(int s) { return 2 * R(s) < 16 ? 16 : 2 * R(s); }
   __host__ __device__ static constexpr int NP(int s) { return KP(s); }
   __host__ __device__ static constexpr int T(int s) { return E / (128 * R(s)); }
@@ -90,13 +94,17 @@ struct Cfg {
 #ifdef TCFFT_NO_BDEDUPE
   __host__ __device__ static constexpr bool BSHARE(int s) { return false; }
 #else
-  __host__ __device__ static constexpr bool BSHARE(int s) { return s >= 2 && R(s) == R(s - 1); }
+  __host__ __device__ static constexpr bool BSHARE(int s) {
+    return (s >= 2 && R(s) == R(s - 1)) || (s == 1 && PLANAR0 && R(1) == R(0));
+  }
 #endif
   __host__ __device__ static constexpr int BOFF(int s) {
     return s == 0 ? 0 : (BSHARE(s) ? BOFF(s - 1) : BOFF(s - 1) + (BSHARE(s - 1) ? 0 : BSZ(s - 1)));
   }
   // writer row-block interleave, plan.cpp writer_groups()
-  __host__ __device__ static constexpr int HSTEP(int s) { return (R(s) > 32 ? 4 : 128 / R(s)) * SBO(s + 1); }
+  __host__ __device__ static constexpr int HSTEP(int s) {
+    return (R(s) <= 32 ? 128 / R(s) : (E / R(s + 1) >= 4 * R(s) ? 4 : 2)) * SBO(s + 1);
+  }
   __host__ __device__ static constexpr int IMOFF(int s) { return 16 * R(s + 1); }
   __host__ __device__ static constexpr int tmax(int a, int b) { return a > b ? a : b; }
   static constexpr int TMAX = tmax(T(0), tmax(T(S > 1 ? 1 : 0), T(S - 1)));
@@ -200,7 +208,18 @@ DEVI void gather_to_tmem(uint32_t s_in, int gbase, int gstride, uint32_t swzmask
     for (int m = 0; m < KC; ++m)
       v[m] = (m < R) ? lds32(s_in + swz((uint32_t)(gbase + m * gs) * 4u, msk)) : 0u;
   }
-  if constexpr (KC == 8) {
+  if constexpr (C::PLANAR0) {
+    // v[m] = (re_m | im_m << 16): column c < KC/2 holds (re_2c, re_2c+1),
+    // column KC/2 + c holds (im_2c, im_2c+1)
+    uint32_t w[KC];
+#pragma unroll
+    for (int c = 0; c < KC / 2; ++c) {
+      w[c] = __byte_perm(v[2 * c], v[2 * c + 1], 0x5410);
+      w[KC / 2 + c] = __byte_perm(v[2 * c], v[2 * c + 1], 0x7632);
+    }
+#pragma unroll
+    for (int q = 0; q < KC / 16; ++q) tmem_st16(taddr + 16 * q, w + 16 * q);
+  } else if constexpr (KC == 8) {
     tmem_st8(taddr, v);
   } else if constexpr (KC == 16) {
     tmem_st16(taddr, v);

@@ -79,7 +79,17 @@ struct Bf {
 
 }  // namespace
 
-int writer_groups(int R) { return R > 32 ? 4 : kLanes / R; }
+int writer_groups(int R, int rows_next) {
+  if (R <= 32) return kLanes / R;
+  return rows_next >= 4 * R ? 4 : 2;  // a super-block of G groups x R rows must fit the next stage
+}
+
+// experiment hook: TCFFT_ROW4096_R64=1 plans 4096-point rows as [64, 64] in
+// 8192-element chunks (two stages, shared planar DFT matrix)
+static bool row4096_r64() {
+  const char* e = std::getenv("TCFFT_ROW4096_R64");
+  return e && std::atoi(e) != 0;
+}
 
 static bool strip_quarter_order() {
   const char* e = std::getenv("TCFFT_STRIP_QUARTER");
@@ -122,6 +132,7 @@ std::vector<int> choose_radices(int n, int kind, bool twiddled) {
   // last stage (fewer, larger MMA tiles, one 64-output epilogue per lane):
   // C4 +1% (round 1).
   // TCFFT_STRIP_R64=0 restores [16, 32] / [32, 32].
+  if (kind == kPassRow && n == 4096 && row4096_r64()) return {64, 64};
   // (2D column strips 1024^2: 0.75 -> 0.83 of roofline)
   if (kind == kPassStrip && !twiddled && (n == 512 || n == 1024)) {
     const char* e2 = std::getenv("TCFFT_STRIP_R64");
@@ -154,6 +165,7 @@ int chunk_elems_for(int n) {
   if (const char* e = std::getenv(key)) return std::atoi(e);
   if (n <= 2) return 1024;
   if (n == 4) return 2048;
+  if (n == 4096 && row4096_r64()) return 8192;
   if (n <= 4096) return 4096;
   return n;  // 8192, 16384: one transform per chunk
 }
@@ -408,7 +420,7 @@ bool build_pass(PassPlan& p, int kind, int N, int64_t count, int64_t images, int
     // writers otherwise put 2 groups x 16 consecutive outputs in a warp: 2-way
     // conflicted strided output stores).  The A region is linear in the row
     // block (tile_bytes == 16 * sbo), so a super-block may span tiles.
-    const int R = st.R, Rn = nx_.R, G = writer_groups(R);
+    const int R = st.R, Rn = nx_.R, G = writer_groups(R, E / Rn);
     const int n2n = st.n2 * R;  // n2 of the next stage
     std::map<std::tuple<int, int, int>, int> gid;
     std::vector<Bf> nxt(E / Rn);
@@ -467,13 +479,16 @@ bool build_pass(PassPlan& p, int kind, int N, int64_t count, int64_t images, int
   }
 
   // ---- B matrices ---------------------------------------------------------
+  // radix-64 first stages use a planar-K TMEM A operand (kernel Cfg::PLANAR0)
+  const bool planar0 = rad[0] == 64;
+  p.planar0 = planar0 ? 1 : 0;
   p.bblob.clear();
   for (int s = 0; s < S; ++s) {
     StageInfo& st = p.st[s];
     const int R = st.R, KP = st.KP, NP = st.NP;
     st.b_bytes = KP * NP * 2;
 #ifndef TCFFT_NO_BDEDUPE
-    if (s >= 2 && p.st[s - 1].R == R) {  // identical planar-K matrix: share it
+    if ((s >= 2 && p.st[s - 1].R == R) || (s == 1 && planar0 && p.st[0].R == R)) {  // identical planar-K matrix: share it
 #else
     if (false) {
 #endif
@@ -487,7 +502,7 @@ bool build_pass(PassPlan& p, int kind, int N, int64_t count, int64_t images, int
         double v = 0.0;
         if (k < 2 * R && n < 2 * R) {
           int m, cin;
-          if (s == 0) {
+          if (s == 0 && !planar0) {
             m = k / 2;
             cin = k % 2;
           } else {

@@ -104,6 +104,7 @@ struct PassPlan {
   int32_t tmem_cols; // allocation (power of two >= 32)
   int32_t tmem_a_cols;
   int32_t ctas_per_sm;
+  int32_t planar0 = 0;       // stage-1 A operand in planar K order (radix-64 first stage)
   int32_t nwg = 1;           // warpgroups per CTA (2 for one-CTA-per-SM passes with even tile counts)
   int32_t a_bufs;            // 1 or 2 A / output-staging buffers
   int32_t tmem_cols_needed;
@@ -126,7 +127,7 @@ struct Plan {
 // Radix list chosen for a single-pass transform of length n (product == n).
 std::vector<int> choose_radices(int n, int kind = kPassRow, bool twiddled = false);
 // row-block interleave of a writer stage of radix R (kernel Cfg::HSTEP mirrors it)
-int writer_groups(int R);
+int writer_groups(int R, int rows_next);
 int chunk_elems_for(int n);
 int pitch_pad_words(int n);
 

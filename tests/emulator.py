@@ -73,7 +73,11 @@ def emulate_chunk(pt: PassTables, chunk_words: np.ndarray, stats: dict | None = 
     w = sbuf[phys // 4]  # (T1, 128, R)
     pairs = w.view(np.float16).reshape(T1, 128, R, 2).astype(np.float64)
     A = np.zeros((T1, 128, KP))
-    A[..., : 2 * R] = pairs.reshape(T1, 128, 2 * R)
+    if d.get("planar0"):  # radix-64 first stage: K = (re_0..re_R-1, im_0..im_R-1)
+        A[..., :R] = pairs[..., 0]
+        A[..., R: 2 * R] = pairs[..., 1]
+    else:  # K = (re_0, im_0, re_1, im_1, ..)
+        A[..., : 2 * R] = pairs.reshape(T1, 128, 2 * R)
     D = A @ pt.bmat(0)
 
     abuf = None

@@ -34,7 +34,7 @@ def test_row_pass_emulation_matches_fft(n):
 
 
 @pytest.mark.parametrize("nx,ny,batch", [(16, 16, 3), (64, 32, 2), (32, 64, 2), (256, 256, 1), (512, 512, 1),
-                                         (1024, 8, 1), (8, 256, 1)])
+                                         (1024, 8, 1), (8, 256, 1), (1024, 64, 1), (2048, 8, 1), (4096, 8, 1)])
 def test_2d_emulation_matches_fft2(nx, ny, batch):
     x = R.random_pairs([9, nx, ny], batch, nx * ny)
     p0 = PassTables(2, nx, ny, batch, 0)
