@@ -133,6 +133,13 @@ std::vector<int> choose_radices(int n, int kind, bool twiddled) {
   // C4 +1% (round 1).
   // TCFFT_STRIP_R64=0 restores [16, 32] / [32, 32].
   if (kind == kPassRow && n == 4096 && row4096_r64()) return {64, 64};
+  // Strided 128-point passes: [8, 16] (two final tiles of 16 outputs per lane
+  // instead of four of 8: fewer per-tile twiddle setups; C3 +2%, round 1).
+  // TCFFT_STRIP128=0 restores [16, 8].
+  if (kind != kPassRow && n == 128) {
+    const char* e3 = std::getenv("TCFFT_STRIP128");
+    if (!e3 || std::atoi(e3) != 0) return {8, 16};
+  }
   // (2D column strips 1024^2: 0.75 -> 0.83 of roofline)
   if (kind == kPassStrip && !twiddled && (n == 512 || n == 1024)) {
     const char* e2 = std::getenv("TCFFT_STRIP_R64");

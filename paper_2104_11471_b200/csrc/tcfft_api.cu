@@ -89,7 +89,8 @@ const KernelEntry kKernels[] = {
     KFOUR(16384, 64, 64, 0, 1),
     // three-step passes A / B (strip + twiddle) of length 64, pass C (strips in,
     // 4D natural-order store out) of length 64 .. 256
-    KENTRY(4096, 8, 8, 0, 4, 1, true),  KENTRY(4096, 8, 8, 0, 4, 3, false), KENTRY(4096, 16, 8, 0, 4, 3, false),
+    KENTRY(4096, 8, 8, 0, 4, 1, true),  KENTRY(4096, 8, 16, 0, 4, 1, true), KENTRY(4096, 8, 16, 0, 4, 3, false),
+    KSTRIP(4096, 8, 16, 0, 4),    KENTRY(4096, 8, 16, 0, 4, 2, false),  KENTRY(4096, 8, 8, 0, 4, 3, false), KENTRY(4096, 16, 8, 0, 4, 3, false),
     KENTRY(4096, 16, 16, 0, 4, 3, false),
     // wider 2D column strips (plan.cpp build_pass; 256: TCFFT_SCHUNK_256 experiment)
     KSTRIP(8192, 16, 32, 0, 2),   KSTRIP(8192, 32, 32, 0, 2),   KSTRIP(16384, 64, 32, 0, 1),
