@@ -113,7 +113,11 @@ struct Cfg {
   static constexpr int OS = N / RL;
   // row passes: 128B-swizzled staging for N == 32 and N >= 2048; 64 <= N <= 1024
   // use padded per-transform staging (plan.cpp pitch_mode) without swizzle
-  static constexpr bool PITCH = ROW_IN && N >= 64 && N <= 1024;
+  // Rows of 64 .. 256 in 4096-element chunks go through the flat 128B-swizzled
+  // map (one TMA box per chunk instead of 16 .. 64 per-row bulk copies: 1D 256
+  // 0.82 -> 0.86 of roofline despite 2-/4-way conflicted gathers / stores);
+  // the small-batch 2048-element chunks (C1) keep the padded pitch (-3% flat).
+  static constexpr bool PITCH = ROW_IN && N >= 64 && N <= 1024 && !(N <= 256 && E_ == 4096);
   static constexpr uint32_t SWZ = (N >= 32 && !PITCH) ? 0x70u : 0u;
   static constexpr bool AFF_IN = ROW_IN && (SWZ == 0 || (GS * 4) % 1024 == 0);
   static constexpr bool AFF_OUT = ROW && (SWZ == 0 || (OS * 4) % 1024 == 0);

@@ -294,7 +294,9 @@ bool build_pass(PassPlan& p, int kind, int N, int64_t count, int64_t images, int
   // Contiguous row inputs with 64 <= N <= 1024 stage each transform at a padded
   // pitch (per-transform bulk copies) so that the lanes of a warp, which span
   // several short transforms, fall into different shared-memory banks.
-  p.pitch_mode = row_in && N >= 64 && N <= 1024;
+  // (kernel Cfg::PITCH mirrors this: rows of 64 .. 256 in 4096-element chunks
+  // use the flat swizzled map instead)
+  p.pitch_mode = row_in && N >= 64 && N <= 1024 && !(N <= 256 && p.E == 4096);
   // strip-in / rows-out passes may stage their output rows at a padded pitch
   // (pitch_pad_words_out)
   p.pitch = p.pitch_mode ? N + pitch_pad_words(N) : (kind == kPassStripT ? N + pitch_pad_words_out(N) : N);  // words
