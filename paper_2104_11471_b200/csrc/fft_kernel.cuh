@@ -351,7 +351,14 @@ DEVI void issue_load(const CUtensorMap* tm, const KIo& io, int T, int64_t chunk,
     return;
   }
   mbar_arrive_expect_tx(bar, (uint32_t)(io.n_sub * io.sub_bytes));
-  if (io.mode == kIoRank1) {
+  if (io.mode == kIoBoxR) {  // whole > 256-row strip in one 4D box
+    const int32_t img = (int32_t)(chunk / io.spi), cb = (int32_t)(chunk % io.spi);
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, "
+        "%5}], [%6];" ::"r"(smem_u32(dst)),
+        "l"(tm), "r"(cb * io.C), "r"(0), "r"(0), "r"(img), "r"(smem_u32(bar))
+        : "memory");
+  } else if (io.mode == kIoRank1) {
     const int32_t e0 = (int32_t)(chunk * io.chunk_rows);
     for (int i = 0; i < io.n_sub; ++i) tma_load_1d(dst + i * io.sub_bytes, tm, e0 + i * io.box_rows, bar);
   } else if (io.mode == kIoFlat) {
@@ -376,6 +383,11 @@ DEVI void issue_store(const CUtensorMap* tm, const KIo& io, int T, int64_t chunk
     const int nt = (int)min((int64_t)T, io.count - t0);
     for (int i = 0; i < nt; ++i)
       bulk_s2g(const_cast<uint8_t*>(io.gptr) + (t0 + i) * io.gstride_bytes, src + i * io.pitch_bytes, io.sub_bytes);
+  } else if (io.mode == kIoBoxR) {
+    const int32_t img = (int32_t)(chunk / io.spi), cb = (int32_t)(chunk % io.spi);
+    asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4}], [%5];" ::"l"(tm),
+                 "r"(cb * io.C), "r"(0), "r"(0), "r"(img), "r"(smem_u32(src))
+                 : "memory");
   } else if (io.mode == kIoRank1) {
     const int32_t e0 = (int32_t)(chunk * io.chunk_rows);
     for (int i = 0; i < io.n_sub; ++i) tma_store_1d(tm, e0 + i * io.box_rows, src + i * io.sub_bytes);

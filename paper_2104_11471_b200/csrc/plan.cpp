@@ -205,6 +205,14 @@ static void box_io(IoDesc& io, int64_t images, int rows, int cols, int C) {
   io.box_rows = std::min(rows, 256);
   io.n_sub = rows / io.box_rows;
   io.sub_bytes = io.box_rows * C * 4;
+  // strips of more than 256 rows: one 4D box ({C, 256, rows/256, 1}) per chunk
+  // instead of rows/256 boxes (TCFFT_BOXR=0 keeps the sub-boxes)
+  const char* e = std::getenv("TCFFT_BOXR");
+  if (rows > 256 && (!e || std::atoi(e) != 0)) {
+    io.mode = kIoBoxR;
+    io.n_sub = 1;
+    io.sub_bytes = rows * C * 4;
+  }
 }
 
 bool build_pass(PassPlan& p, int kind, int N, int64_t count, int64_t images, int cols, std::string* err,
@@ -349,7 +357,7 @@ bool build_pass(PassPlan& p, int kind, int N, int64_t count, int64_t images, int
   }
   p.swz_in = p.in.swz;
   p.swz_out = p.out.swz;
-  p.flat = p.in.mode != kIoBox;
+  p.flat = p.in.mode != kIoBox && p.in.mode != kIoBoxR;
   p.total = p.in.total;
 
   int n2 = 1, tiles_max = 0;

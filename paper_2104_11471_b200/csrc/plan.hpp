@@ -30,6 +30,7 @@ enum IoMode : int32_t {
   kIoFlat = 1,   // 2D tensor map [total/W][W] over a contiguous chunk
   kIoRank1 = 2,  // 1D tensor map [total] in 256-element boxes
   kIoPitch = 3,  // per-transform 1D bulk copies into a padded staging pitch
+  kIoBoxR = 4,   // 4D tensor map {C, 256, rows/256, 1}: a > 256-row strip in ONE box
 };
 
 // How one side (load or store) of a pass moves a chunk between HBM and SMEM.

@@ -259,6 +259,20 @@ tcfftResult make_tmap(CUtensorMap* tm, const tcfft::IoDesc& io, const void* base
     r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<void*>(base), dims, strides, box, es,
             CU_TENSOR_MAP_INTERLEAVE_NONE, io.W == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  } else if (io.mode == tcfft::kIoBoxR) {
+    const int k = io.rows / 256;
+    cuuint64_t dims[4] = {(cuuint64_t)io.cols, 256, (cuuint64_t)k, (cuuint64_t)io.images};
+    cuuint64_t strides[3] = {(cuuint64_t)io.cols * 4, (cuuint64_t)io.cols * 256 * 4,
+                             (cuuint64_t)io.cols * io.rows * 4};
+    cuuint32_t box[4] = {(cuuint32_t)io.C, 256, (cuuint32_t)k, 1};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    const int run = io.C * 4;
+    CUtensorMapSwizzle sw = run == 128  ? CU_TENSOR_MAP_SWIZZLE_128B
+                            : run == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                            : run == 32 ? CU_TENSOR_MAP_SWIZZLE_32B
+                                        : CU_TENSOR_MAP_SWIZZLE_NONE;
+    r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, const_cast<void*>(base), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   } else {
     const int64_t rs = io.row_stride ? io.row_stride : io.cols;
     const int64_t is = io.img_stride ? io.img_stride : (int64_t)io.cols * io.rows;
@@ -318,7 +332,7 @@ void build_fused(tcfftPlanImpl* h, const cudaDeviceProp& prop) {
   if (h->plan.passes.size() != 2 || h->plan.dims != 2) return;
   const PassPlan& A = h->plan.passes[0];
   const PassPlan& B = h->plan.passes[1];
-  if (B.IMG != 1 || B.in.mode != tcfft::kIoBox) return;  // column strips of one image per chunk
+  if (B.IMG != 1 || (B.in.mode != tcfft::kIoBox && B.in.mode != tcfft::kIoBoxR)) return;  // column strips of one image per chunk
   const int64_t objs = h->plan.batch;
   const int64_t rows_per_obj = h->plan.nx;             // pass A: rows of length ny
   if (rows_per_obj % A.T) return;
