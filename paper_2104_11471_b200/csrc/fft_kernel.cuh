@@ -351,7 +351,13 @@ DEVI void issue_load(const CUtensorMap* tm, const KIo& io, int T, int64_t chunk,
     return;
   }
   mbar_arrive_expect_tx(bar, (uint32_t)(io.n_sub * io.sub_bytes));
-  if (io.mode == kIoBoxR) {  // whole > 256-row strip in one 4D box
+  if (io.mode == kIoFlat3) {  // whole > 256-row flat chunk in one 3D box
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+        "[%5];" ::"r"(smem_u32(dst)),
+        "l"(tm), "r"(0), "r"(0), "r"((int32_t)(chunk * io.n_sub)), "r"(smem_u32(bar))
+        : "memory");
+  } else if (io.mode == kIoBoxR) {  // whole > 256-row strip in one 4D box
     const int32_t img = (int32_t)(chunk / io.spi), cb = (int32_t)(chunk % io.spi);
     asm volatile(
         "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, "
@@ -383,6 +389,10 @@ DEVI void issue_store(const CUtensorMap* tm, const KIo& io, int T, int64_t chunk
     const int nt = (int)min((int64_t)T, io.count - t0);
     for (int i = 0; i < nt; ++i)
       bulk_s2g(const_cast<uint8_t*>(io.gptr) + (t0 + i) * io.gstride_bytes, src + i * io.pitch_bytes, io.sub_bytes);
+  } else if (io.mode == kIoFlat3) {
+    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(tm),
+                 "r"(0), "r"(0), "r"((int32_t)(chunk * io.n_sub)), "r"(smem_u32(src))
+                 : "memory");
   } else if (io.mode == kIoBoxR) {
     const int32_t img = (int32_t)(chunk / io.spi), cb = (int32_t)(chunk % io.spi);
     asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4}], [%5];" ::"l"(tm),

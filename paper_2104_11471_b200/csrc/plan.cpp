@@ -190,6 +190,10 @@ static void flat_io(IoDesc& io, int64_t total, int E, bool allow_swizzle) {
   io.sub_bytes = io.box_rows * io.W * 4;
   io.chunk_rows = E / io.W;
   io.total = total;
+  // chunks of more than 256 rows: one 3D box instead of n_sub 2D boxes
+  const char* e = std::getenv("TCFFT_FLAT3");
+  if (io.mode == kIoFlat && io.n_sub > 1 && (total / io.W) % 256 == 0 && (!e || std::atoi(e) != 0))
+    io.mode = kIoFlat3;
 }
 
 // 3D column-box TMA view of an images x rows x cols array, C columns per chunk.

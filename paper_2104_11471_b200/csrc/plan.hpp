@@ -31,6 +31,7 @@ enum IoMode : int32_t {
   kIoRank1 = 2,  // 1D tensor map [total] in 256-element boxes
   kIoPitch = 3,  // per-transform 1D bulk copies into a padded staging pitch
   kIoBoxR = 4,   // 4D tensor map {C, 256, rows/256, 1}: a > 256-row strip in ONE box
+  kIoFlat3 = 5,  // 3D tensor map {W, 256, n_sub} over [total/W/256][256][W]: one box per chunk
 };
 
 // How one side (load or store) of a pass moves a chunk between HBM and SMEM.

@@ -259,6 +259,14 @@ tcfftResult make_tmap(CUtensorMap* tm, const tcfft::IoDesc& io, const void* base
     r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<void*>(base), dims, strides, box, es,
             CU_TENSOR_MAP_INTERLEAVE_NONE, io.W == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  } else if (io.mode == tcfft::kIoFlat3) {
+    cuuint64_t dims[3] = {(cuuint64_t)io.W, 256, (cuuint64_t)(io.total / io.W / 256)};
+    cuuint64_t strides[2] = {(cuuint64_t)io.W * 4, (cuuint64_t)io.W * 256 * 4};
+    cuuint32_t box[3] = {(cuuint32_t)io.W, 256, (cuuint32_t)io.n_sub};
+    cuuint32_t es[3] = {1, 1, 1};
+    r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, const_cast<void*>(base), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, io.W == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   } else if (io.mode == tcfft::kIoBoxR) {
     const int k = io.rows / 256;
     cuuint64_t dims[4] = {(cuuint64_t)io.cols, 256, (cuuint64_t)k, (cuuint64_t)io.images};
