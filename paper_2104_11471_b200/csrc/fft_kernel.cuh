@@ -67,13 +67,15 @@ using namespace sm100;
 
 // ---------------------------------------------------------------- compile-time pass geometry
 // kModeStrip4: column strips in, 4D tensor-map store out (three-step pass C)
-enum : int { kModeRow = 0, kModeStrip = 1, kModeRowT = 2, kModeStrip4 = 3 };
+// kModeRowU: rows of 4 .. 16 whose batch is not a multiple of 32 elements
+// (unswizzled [total/4][4] staging)
+enum : int { kModeRow = 0, kModeStrip = 1, kModeRowT = 2, kModeStrip4 = 3, kModeRowU = 5 };
 
 template <int E_, int R1_, int R2_, int R3_, int MODE_>
 struct Cfg {
   static constexpr int E = E_;
-  static constexpr bool ROW_IN = MODE_ == kModeRow || MODE_ == kModeRowT;  // contiguous rows in (compile-time strides)
-  static constexpr bool ROW = MODE_ == kModeRow;        // ... and contiguous rows out
+  static constexpr bool ROW_IN = MODE_ == kModeRow || MODE_ == kModeRowT || MODE_ == kModeRowU;  // contiguous rows in
+  static constexpr bool ROW = MODE_ == kModeRow || MODE_ == kModeRowU;  // ... and contiguous rows out
   static constexpr int S = (R2_ == 0) ? 1 : ((R3_ == 0) ? 2 : 3);
   static constexpr int N = R1_ * (R2_ ? R2_ : 1) * (R3_ ? R3_ : 1);
   __host__ __device__ static constexpr int R(int s) { return s == 0 ? R1_ : (s == 1 ? R2_ : R3_); }
@@ -118,7 +120,9 @@ struct Cfg {
   // 0.82 -> 0.86 of roofline despite 2-/4-way conflicted gathers / stores);
   // the small-batch 2048-element chunks (C1) keep the padded pitch (-3% flat).
   static constexpr bool PITCH = ROW_IN && N >= 64 && N <= 1024 && !(N <= 256 && E_ == 4096);
-  static constexpr uint32_t SWZ = (N >= 32 && !PITCH) ? 0x70u : 0u;
+  // (rows of 4 .. 16 too: each lane owns one whole transform, and the swizzle
+  // spreads the lanes' N-word strides over the banks: 16-way -> 2-way at N = 16)
+  static constexpr uint32_t SWZ = (N >= 4 && !PITCH && MODE_ != kModeRowU) ? 0x70u : 0u;
   static constexpr bool AFF_IN = ROW_IN && (SWZ == 0 || (GS * 4) % 1024 == 0);
   static constexpr bool AFF_OUT = ROW && (SWZ == 0 || (OS * 4) % 1024 == 0);
   // TMEM: D region (max over stages) then the stage-1 A region

@@ -335,9 +335,9 @@ bool build_pass(PassPlan& p, int kind, int N, int64_t count, int64_t images, int
       p.in.sub_bytes = N * 4;
       p.in.total = total;
     } else {
-      // row passes with N < 32 stay unswizzled: the kernel's compile-time row
-      // addressing assumes the 128B swizzle exactly when N == 32 or N >= 2048
-      flat_io(p.in, total, E, N >= 32);
+      // 128B-swizzled [total/32][32] view for N >= 4 (kernel Cfg::SWZ mirrors
+      // this; N = 2 keeps the plain view)
+      flat_io(p.in, total, E, N >= 4);
     }
   } else if (p.C == cols) {
     flat_io(p.in, images * (int64_t)N * cols, E, true);

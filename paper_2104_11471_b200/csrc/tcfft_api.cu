@@ -101,6 +101,8 @@ const KernelEntry kKernels[] = {
     KENTRYW(16384, 64, 32, 0, 1, 1, false, 2),
     // column strips of 256 columns for N <= 8 (2D nx <= 8 with ny > 256)
     KSTRIP(512, 2, 0, 0, 4),      KSTRIP(1024, 4, 0, 0, 4),     KSTRIP(2048, 8, 0, 0, 4),
+    // rows of 4 .. 16 whose element count is not a multiple of 32 (unswizzled staging)
+    KENTRY(2048, 4, 0, 0, 4, 5, false), KENTRY(4096, 8, 0, 0, 4, 5, false), KENTRY(4096, 16, 0, 0, 4, 5, false),
     // small-batch row passes (half chunks, plan.cpp build_pass)
     KROW(2048, 16, 16, 0, 4),     KROW(2048, 16, 8, 0, 4),      KROW(2048, 8, 8, 0, 4),
 };
@@ -112,6 +114,7 @@ const KernelEntry* find_kernel(const PassPlan& p) {
   // passes run the strip kernel (their output addressing is all runtime)
   const int mode = p.kind == tcfft::kPassStripT                          ? (int)tcfft::kPassStrip
                    : (p.kind == tcfft::kPassStrip && p.out.img_split)  ? 3 /* kModeStrip4 */
+                   : (p.kind == tcfft::kPassRow && p.N >= 4 && p.N < 32 && p.in.W != 32) ? 5 /* kModeRowU */
                                                                         : p.kind;
   const int tw4 = p.tw4_total ? 1 : 0;
   // the planner's warpgroup count if that instantiation exists, else one
