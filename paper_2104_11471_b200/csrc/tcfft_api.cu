@@ -516,7 +516,13 @@ tcfftResult create(tcfftHandle* out, int dims, int nx, int ny, int batch) {
     int64_t slots = (int64_t)prop.multiProcessorCount * p.ctas_per_sm;
     d.grid = (int)std::min<int64_t>(p.chunks, slots);
     k.static_chunks = d.grid;
-    if (k.ctr && dyn_mode == 2) k.static_chunks = std::max<int64_t>(d.grid, (p.chunks / d.grid - 2) * d.grid);
+    if (k.ctr && dyn_mode == 2) {
+      static const int tail = [] {  // ticketed rounds at the end (experiment hook TCFFT_DYN_TAIL)
+        const char* e = std::getenv("TCFFT_DYN_TAIL");
+        return e ? std::max(1, std::atoi(e)) : 2;
+      }();
+      k.static_chunks = std::max<int64_t>(d.grid, (p.chunks / d.grid - tail) * d.grid);
+    }
 #ifdef TCFFT_TRACE
     cudaMalloc(reinterpret_cast<void**>(&d.kp.trace), (size_t)d.grid * 8 * sizeof(unsigned long long));
 #endif
