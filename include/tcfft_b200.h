@@ -48,11 +48,13 @@ tcfftResult tcfftPlan1D(tcfftHandle* plan, int nx, int batch);
 tcfftResult tcfftPlan2D(tcfftHandle* plan, int nx, int ny, int batch);
 /* Stream for subsequent executions (cudaStream_t passed as void*; NULL = legacy default). */
 tcfftResult tcfftSetStream(tcfftHandle plan, void* stream);
-/* Concurrency: executions are ordered on the plan's stream.  A plan without a
- * workspace (tcfftGetWorkspaceSize == 0: 1D N <= 16384 and all 2D plans) may
- * be executed on several streams concurrently (different buffers; set the
- * stream and execute under one host lock).  Plans with a workspace (1D N >
- * 16384) run one execution at a time: use one plan per stream. */
+/* Concurrency: executions are ordered on the plan's stream.  tcfftExecC2C on
+ * a plan without a workspace (tcfftGetWorkspaceSize == 0: 1D N <= 16384 and
+ * all 2D plans) may run on several streams concurrently (different buffers;
+ * set the stream and execute under one host lock).  Plans with a workspace
+ * (1D N > 16384), tcfftExecC2CHost and the scratch path of
+ * tcfftExecC2CStrided use plan-owned device memory and run one execution at a
+ * time: use one plan per stream for those. */
 /* Bytes of device workspace the plan owns (0 for single-pass plans). */
 tcfftResult tcfftGetWorkspaceSize(tcfftHandle plan, size_t* bytes);
 /* Forward FP16 C2C transform; idata/odata are device pointers to __half2
