@@ -54,7 +54,9 @@ tcfftResult tcfftSetStream(tcfftHandle plan, void* stream);
  * set the stream and execute under one host lock).  Plans with a workspace
  * (1D N > 16384), tcfftExecC2CHost and the scratch path of
  * tcfftExecC2CStrided use plan-owned device memory and run one execution at a
- * time: use one plan per stream for those. */
+ * time: use one plan per stream for those.  Every exec entry point returns
+ * TCFFT_INVALID_VALUE when the calling thread's current device is not the
+ * device the plan was created on. */
 /* Bytes of device workspace the plan owns (0 for single-pass plans). */
 tcfftResult tcfftGetWorkspaceSize(tcfftHandle plan, size_t* bytes);
 /* Forward FP16 C2C transform; idata/odata are device pointers to __half2

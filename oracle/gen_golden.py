@@ -3,12 +3,17 @@
 TEST INFRASTRUCTURE ONLY (see oracle/restate.py header).  Run in the build
 container, where the read-only reference lives:
 
-    python oracle/gen_golden.py [--ref /root/reference/pkg/src]
+    python oracle/gen_golden.py [--ref /root/reference/pkg/src] [--ext baseline/_ref]
 
 The reference is imported as-is (``tcfft`` package, reference
-``pkg/src/tcfft/__init__.py``); its pure-python MMA backend is selected
-(``TCFFT_BACKEND=py``, ``backend.py:33-45``), which the reference's own tests
-prove bit-identical to the compiled one (``tests/test_backends.py:30-60``).
+``pkg/src/tcfft/__init__.py``).  Small cases run its pure-python MMA backend
+(``TCFFT_BACKEND=py``, ``backend.py:33-45``); the large hash-only cases (1D
+2^17 .. 2^24, 2D 1024x512 .. 4096^2) run its compiled Cython backend
+(``TCFFT_BACKEND=ext``, ``_core.pyx``) from the unmodified install in
+``baseline/_ref`` (``pip install --no-deps --target baseline/_ref`` of a copy
+of ``/root/reference/pkg``), which the reference's own tests prove
+bit-identical to the python one (``tests/test_backends.py:30-60``).  Cases run
+in parallel worker processes (one reference process per case).
 Inputs follow the reference CLI protocol (seeded U[-1,1) re/im rounded to fp16,
 ``cli.py:40-43``).  Outputs are stored as raw fp16 pairs; large cases store a
 SHA-256 of the output bytes instead of the bytes.
@@ -37,6 +42,9 @@ CASES_1D = [(n, b) for n, b in [
     (32768, 1), (65536, 1)]]
 CASES_2D = [(2, 2, 2), (16, 16, 2), (32, 64, 1), (64, 32, 1), (256, 256, 1),
             (512, 256, 1)]
+# large cases: SHA-256 only (the reference's ext backend; minutes each)
+CASES_1D_BIG = [(1 << k, 1) for k in range(17, 25)]
+CASES_2D_BIG = [(1024, 512, 1), (1024, 1024, 1), (2048, 2048, 1), (4096, 4096, 1)]
 STORE_LIMIT = 1 << 15  # elements per case stored verbatim; above: hash only
 
 
@@ -44,37 +52,55 @@ def _sha(a: np.ndarray) -> str:
     return hashlib.sha256(np.ascontiguousarray(a).view(np.uint16).tobytes()).hexdigest()
 
 
+def _run_case(job):
+    """One reference execution in a fresh worker process (job = (tag, nx, ny,
+    batch, cfg, backend, src))."""
+    tag, nx, ny, batch, cfg, backend, src = job
+    os.environ["TCFFT_BACKEND"] = backend
+    sys.path.insert(0, src)
+    import tcfft  # the reference package
+
+    assert tcfft.backend.active_backend() == backend, (tcfft.__file__, backend)
+    total = nx * (ny or 1)
+    x = random_pairs([cfg, 0], batch, total)
+    data = tcfft.BatchedTensor(x.reshape(-1, 2).copy(), batch, total)
+    plan = tcfft.plan_1d(nx, batch) if ny is None else tcfft.plan_2d(nx, ny, batch)
+    tcfft.execute(plan, data)
+    y = data.pairs.reshape(batch, total, 2)
+    return f"{tag}|{nx}|{ny or 0}|{batch}|{cfg}|{_sha(y)}", (y if batch * total <= STORE_LIMIT else None)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--ref", default="/root/reference/pkg/src")
+    ap.add_argument("--ext", default=str(ROOT / "baseline" / "_ref"))
     ap.add_argument("--out", default=str(ROOT / "tests" / "golden"))
+    ap.add_argument("--jobs", type=int, default=len(os.sched_getaffinity(0)))
     args = ap.parse_args()
-    os.environ.setdefault("TCFFT_BACKEND", "py")
-    sys.path.insert(0, args.ref)
-    import tcfft  # the reference package
+    import multiprocessing as mp
 
     out = Path(args.out)
     out.mkdir(parents=True, exist_ok=True)
     store = {}
     meta = []
-
-    def run(tag, nx, ny, batch, cfg):
-        total = nx * (ny or 1)
-        x = random_pairs([cfg, 0], batch, total)
-        data = tcfft.BatchedTensor(x.reshape(-1, 2).copy(), batch, total)
-        plan = tcfft.plan_1d(nx, batch) if ny is None else tcfft.plan_2d(nx, ny, batch)
-        tcfft.execute(plan, data)
-        y = data.pairs.reshape(batch, total, 2)
-        rec = f"{tag}|{nx}|{ny or 0}|{batch}|{cfg}|{_sha(y)}"
+    jobs = [("1d", n, None, b, 100 + i, "py", args.ref) for i, (n, b) in enumerate(CASES_1D)]
+    jobs += [("2d", nx, ny, b, 200 + i, "py", args.ref) for i, (nx, ny, b) in enumerate(CASES_2D)]
+    jobs += [("1d", n, None, b, 300 + i, "ext", args.ext) for i, (n, b) in enumerate(CASES_1D_BIG)]
+    jobs += [("2d", nx, ny, b, 400 + i, "ext", args.ext) for i, (nx, ny, b) in enumerate(CASES_2D_BIG)]
+    # longest first, so the pool's tail is short
+    order = sorted(range(len(jobs)), key=lambda i: -jobs[i][1] * (jobs[i][2] or 1) * jobs[i][3])
+    with mp.get_context("spawn").Pool(args.jobs, maxtasksperchild=1) as pool:
+        res = dict(zip(order, pool.map(_run_case, [jobs[i] for i in order], chunksize=1)))
+    for i, job in enumerate(jobs):
+        rec, y = res[i]
         meta.append(rec)
-        if batch * total <= STORE_LIMIT:
-            store[f"{tag}_{nx}_{ny or 0}_out"] = y
+        if y is not None:
+            store[f"{job[0]}_{job[1]}_{job[2] or 0}_out"] = y
         print(rec, flush=True)
 
-    for i, (n, b) in enumerate(CASES_1D):
-        run("1d", n, None, b, 100 + i)
-    for i, (nx, ny, b) in enumerate(CASES_2D):
-        run("2d", nx, ny, b, 200 + i)
+    os.environ["TCFFT_BACKEND"] = "py"
+    sys.path.insert(0, args.ref)
+    import tcfft  # the reference package (KATs below)
 
     # Known-answer vectors from the reference's own tests.
     kat = {}

@@ -17,6 +17,7 @@ from __future__ import annotations
 import ctypes
 import json
 import math
+import threading
 from dataclasses import dataclass, field
 from functools import reduce
 
@@ -105,6 +106,11 @@ class Plan:
     precision: str = "half"
     _handle: object = field(default=None, repr=False)
     _desc: dict = field(default_factory=dict, repr=False)
+    _device: int = field(default=-1, repr=False)
+    # tcfftSetStream + exec form one critical section (include/tcfft_b200.h):
+    # ctypes releases the GIL, so two threads sharing a plan would otherwise
+    # launch on each other's stream
+    _lock: object = field(default_factory=threading.Lock, repr=False)
 
     @property
     def n_logical(self) -> int:
@@ -139,6 +145,15 @@ class Plan:
             pass
 
 
+def _current_device() -> int:
+    try:
+        import torch
+
+        return torch.cuda.current_device() if torch.cuda.is_available() else -1
+    except Exception:
+        return -1
+
+
 def _create(dims, nx, ny, batch):
     L = _lib.load()
     h = ctypes.c_void_p()
@@ -161,7 +176,7 @@ def plan_1d(nx: int, batch: int, *, continuous_size: int = 32, precision: str = 
     sched = schedule_radices(nx) if schedule is None else _validate_schedule(schedule, nx)
     desc = _lib.describe(1, nx, 0, batch)
     h = _create(1, nx, 0, batch)
-    return Plan(1, nx, None, batch, sched, None, continuous_size, precision, h, desc)
+    return Plan(1, nx, None, batch, sched, None, continuous_size, precision, h, desc, _current_device())
 
 
 def plan_2d(nx: int, ny: int, batch: int, *, continuous_size: int = 32, precision: str = "half") -> Plan:
@@ -172,7 +187,8 @@ def plan_2d(nx: int, ny: int, batch: int, *, continuous_size: int = 32, precisio
     _common_checks(batch, continuous_size, precision)
     desc = _lib.describe(2, nx, ny, batch)
     h = _create(2, nx, ny, batch)
-    return Plan(2, nx, ny, batch, schedule_radices(nx), schedule_radices(ny), continuous_size, precision, h, desc)
+    return Plan(2, nx, ny, batch, schedule_radices(nx), schedule_radices(ny), continuous_size, precision, h, desc,
+                _current_device())
 
 
 def _as_pairs(t):
@@ -197,6 +213,11 @@ def _as_pairs(t):
     if t.data_ptr() % 16:
         raise ExecuteError("data must be 16-byte aligned")
     return t, n
+
+
+def _check_device(plan: Plan, t) -> None:
+    if plan._device >= 0 and t.device.index != plan._device:
+        raise ExecuteError(f"data is on {t.device}, the plan was created on cuda:{plan._device}")
 
 
 def execute(plan: Plan, data, out=None, stream=None):
@@ -225,9 +246,10 @@ def execute(plan: Plan, data, out=None, stream=None):
             raise ExecuteError("out must hold as many elements as data")
         if o.device != t.device:
             raise ExecuteError("data and out must be on the same device")
+    _check_device(plan, t)
     L = _lib.load()
     s = stream if stream is not None else torch.cuda.current_stream(t.device)
-    with torch.cuda.device(t.device):
+    with torch.cuda.device(t.device), plan._lock:
         st = L.tcfftSetStream(plan._handle, ctypes.c_void_p(s.cuda_stream))
         if st == _lib.TCFFT_SUCCESS:
             st = L.tcfftExecC2C(plan._handle, ctypes.c_void_p(t.data_ptr()), ctypes.c_void_p(o.data_ptr()))
@@ -248,9 +270,10 @@ def _execute_view(plan: Plan, data, stream=None):
     t = data.pairs
     if not t.is_cuda or t.dtype != torch.float16 or not t.is_contiguous():
         raise ExecuteError("BatchedTensor pairs must be a contiguous float16 CUDA tensor")
+    _check_device(plan, t)
     L = _lib.load()
     s = stream if stream is not None else torch.cuda.current_stream(t.device)
-    with torch.cuda.device(t.device):
+    with torch.cuda.device(t.device), plan._lock:
         st = L.tcfftSetStream(plan._handle, ctypes.c_void_p(s.cuda_stream))
         if st == _lib.TCFFT_SUCCESS:
             ptr = ctypes.c_void_p(t.data_ptr())
@@ -269,20 +292,27 @@ def execute_host(plan: Plan, data, out=None, stream=None):
 
     if plan._handle is None:
         raise ExecuteError("plan has been destroyed")
-    for t in (data,) + ((out,) if out is not None else ()):
+    need = plan.batch * plan.n_logical
+    for what, t in (("data", data),) + ((("out", out),) if out is not None else ()):
         if not isinstance(t, torch.Tensor) or t.is_cuda:
             raise ExecuteError("execute_host needs CPU (host) tensors")
         if t.dtype not in (torch.complex32, torch.float16) or not t.is_contiguous():
             raise ExecuteError("host data must be contiguous complex32 / float16[..., 2]")
-    n = data.numel() // (1 if data.dtype == torch.complex32 else 2)
-    if n != plan.batch * plan.n_logical:
-        raise ExecuteError(f"data holds {n} complex elements, plan needs {plan.batch * plan.n_logical}")
+        if t.dtype == torch.float16 and (t.dim() == 0 or t.shape[-1] != 2):
+            raise ExecuteError(f"float16 {what} must have a trailing dimension of 2 (re, im), got {tuple(t.shape)}")
+        # tcfftExecC2CHost reads and writes batch * len * 4 bytes: an undersized
+        # buffer would be overrun
+        n = t.numel() // (1 if t.dtype == torch.complex32 else 2)
+        if n != need:
+            raise ExecuteError(f"{what} holds {n} complex elements, plan needs {need}")
     o = data if out is None else out
     L = _lib.load()
-    s = stream if stream is not None else torch.cuda.current_stream()
-    st = L.tcfftSetStream(plan._handle, ctypes.c_void_p(s.cuda_stream))
-    if st == _lib.TCFFT_SUCCESS:
-        st = L.tcfftExecC2CHost(plan._handle, ctypes.c_void_p(data.data_ptr()), ctypes.c_void_p(o.data_ptr()))
+    dev = plan._device if plan._device >= 0 else torch.cuda.current_device()
+    s = stream if stream is not None else torch.cuda.current_stream(dev)
+    with torch.cuda.device(dev), plan._lock:
+        st = L.tcfftSetStream(plan._handle, ctypes.c_void_p(s.cuda_stream))
+        if st == _lib.TCFFT_SUCCESS:
+            st = L.tcfftExecC2CHost(plan._handle, ctypes.c_void_p(data.data_ptr()), ctypes.c_void_p(o.data_ptr()))
     if st != _lib.TCFFT_SUCCESS:
         raise ExecuteError(f"tcfftExecC2CHost failed: {_lib.error_string(st)}")
     s.synchronize()

@@ -17,7 +17,8 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libtcfft_b200.so"
 SOURCES = [CSRC / "tcfft_api.cu", CSRC / "plan.cpp"]
-DEPS = SOURCES + [CSRC / "fft_kernel.cuh", CSRC / "sm100.cuh", CSRC / "plan.hpp", ROOT / "include" / "tcfft_b200.h"]
+# every source and header the library is built from (a stale .so must never load)
+DEPS = SOURCES + sorted(CSRC.glob("*.cuh")) + sorted(CSRC.glob("*.hpp")) + sorted((ROOT / "include").glob("*.h"))
 
 
 def nvcc() -> str:

@@ -79,6 +79,11 @@ struct Bf {
 
 }  // namespace
 
+const char* experiment_env(const char* name) {
+  const char* e = std::getenv("TCFFT_EXPERIMENTS");
+  return (e && std::atoi(e) == 1) ? std::getenv(name) : nullptr;
+}
+
 int writer_groups(int R, int rows_next) {
   if (R <= 32) return kLanes / R;
   return rows_next >= 4 * R ? 4 : 2;  // a super-block of G groups x R rows must fit the next stage
@@ -87,12 +92,12 @@ int writer_groups(int R, int rows_next) {
 // experiment hook: TCFFT_ROW4096_R64=1 plans 4096-point rows as [64, 64] in
 // 8192-element chunks (two stages, shared planar DFT matrix)
 static bool row4096_r64() {
-  const char* e = std::getenv("TCFFT_ROW4096_R64");
+  const char* e = experiment_env("TCFFT_ROW4096_R64");
   return e && std::atoi(e) != 0;
 }
 
 static bool strip_quarter_order() {
-  const char* e = std::getenv("TCFFT_STRIP_QUARTER");
+  const char* e = experiment_env("TCFFT_STRIP_QUARTER");
   return !e || std::atoi(e) != 0;
 }
 
@@ -102,14 +107,14 @@ static bool strip_quarter_order() {
 // one bulk copy per row: measured 23.3 vs 20.6 TFLOP/s for C3 (N = 128,
 // round 1), so dense unless the conflicts get worse than 2-way.
 static int pitch_pad_words_out(int n) {
-  const char* e = std::getenv("TCFFT_STRIPT_PAD");
+  const char* e = experiment_env("TCFFT_STRIPT_PAD");
   if (e) return std::atoi(e);
   return n <= 128 ? 0 : 8;
 }
 
 int pitch_pad_words(int n) {
   // chosen with tests/emulator.py's bank model (see test_plan_emulation.py)
-  const char* e = std::getenv("TCFFT_PITCH_PAD");
+  const char* e = experiment_env("TCFFT_PITCH_PAD");
   if (e) return std::atoi(e);
   return (n >= 64 && n <= 1024) ? 8 : 0;
 }
@@ -122,7 +127,7 @@ std::vector<int> choose_radices(int n, int kind, bool twiddled) {
   // (8-way conflicted output stores, tests/emulator.py).  With two stages the
   // final k run is consecutive.  Radix-64 stage 1 reads its A operand from
   // TMEM, so the larger DFT block costs no extra shared-memory traffic.
-  const char* e = std::getenv("TCFFT_STRIDED_R64");
+  const char* e = experiment_env("TCFFT_STRIDED_R64");
   const bool r64 = !e || std::atoi(e) != 0;
   if (kind != kPassRow && r64) {
     if (n == 2048) return {64, 32};
@@ -137,12 +142,12 @@ std::vector<int> choose_radices(int n, int kind, bool twiddled) {
   // instead of four of 8: fewer per-tile twiddle setups; C3 +2%, round 1).
   // TCFFT_STRIP128=0 restores [16, 8].
   if (kind != kPassRow && n == 128) {
-    const char* e3 = std::getenv("TCFFT_STRIP128");
+    const char* e3 = experiment_env("TCFFT_STRIP128");
     if (!e3 || std::atoi(e3) != 0) return {8, 16};
   }
   // (2D column strips 1024^2: 0.75 -> 0.83 of roofline)
   if (kind == kPassStrip && !twiddled && (n == 512 || n == 1024)) {
-    const char* e2 = std::getenv("TCFFT_STRIP_R64");
+    const char* e2 = experiment_env("TCFFT_STRIP_R64");
     const int v = e2 ? std::atoi(e2) : 1;
     if (v) return n == 512 ? std::vector<int>{8, 64} : std::vector<int>{16, 64};
   }
@@ -169,7 +174,7 @@ int chunk_elems_for(int n) {
   // experiment hook: TCFFT_CHUNK_<n>=<elems> overrides the chunk size
   char key[32];
   std::snprintf(key, sizeof(key), "TCFFT_CHUNK_%d", n);
-  if (const char* e = std::getenv(key)) return std::atoi(e);
+  if (const char* e = experiment_env(key)) return std::atoi(e);
   if (n <= 2) return 1024;
   if (n == 4) return 2048;
   if (n == 4096 && row4096_r64()) return 8192;
@@ -191,7 +196,7 @@ static void flat_io(IoDesc& io, int64_t total, int E, bool allow_swizzle) {
   io.chunk_rows = E / io.W;
   io.total = total;
   // chunks of more than 256 rows: one 3D box instead of n_sub 2D boxes
-  const char* e = std::getenv("TCFFT_FLAT3");
+  const char* e = experiment_env("TCFFT_FLAT3");
   if (io.mode == kIoFlat && io.n_sub > 1 && (total / io.W) % 256 == 0 && (!e || std::atoi(e) != 0))
     io.mode = kIoFlat3;
 }
@@ -211,7 +216,7 @@ static void box_io(IoDesc& io, int64_t images, int rows, int cols, int C) {
   io.sub_bytes = io.box_rows * C * 4;
   // strips of more than 256 rows: one 4D box ({C, 256, rows/256, 1}) per chunk
   // instead of rows/256 boxes (TCFFT_BOXR=0 keeps the sub-boxes)
-  const char* e = std::getenv("TCFFT_BOXR");
+  const char* e = experiment_env("TCFFT_BOXR");
   if (rows > 256 && (!e || std::atoi(e) != 0)) {
     io.mode = kIoBoxR;
     io.n_sub = 1;
@@ -239,7 +244,7 @@ bool build_pass(PassPlan& p, int kind, int N, int64_t count, int64_t images, int
     // are latency bound: halve the chunk so each CTA's load -> 2 MMA stages ->
     // store chain is shorter and twice as many CTAs share the work (C1
     // N=256 x 4096: 7.2 -> 8.1 TFLOP/s, round 1).
-    const char* ce = std::getenv("TCFFT_SMALL_CHUNK");
+    const char* ce = experiment_env("TCFFT_SMALL_CHUNK");
     if ((!ce || std::atoi(ce) != 0) && p.E == 4096 && N >= 64 && N <= 256 &&
         (count * (int64_t)N + 4095) / 4096 < 148 * 4)
       p.E = 2048;
@@ -274,7 +279,7 @@ bool build_pass(PassPlan& p, int kind, int N, int64_t count, int64_t images, int
     {
       char key[32];  // experiment hook: TCFFT_SCHUNK_<n>=<elems> overrides the strip chunk size
       std::snprintf(key, sizeof(key), "TCFFT_SCHUNK_%d", N);
-      if (const char* e = std::getenv(key)) p.E = std::atoi(e);
+      if (const char* e = experiment_env(key)) p.E = std::atoi(e);
     }
     int ci = p.E / N;  // C * IMG
     if (ci <= cols) {
@@ -578,7 +583,7 @@ bool build_pass(PassPlan& p, int kind, int N, int64_t count, int64_t images, int
     (void)fixed;
     (void)tmem_ctas;
 #endif
-    if (const char* e = std::getenv("TCFFT_ABUFS")) p.a_bufs = std::max(1, std::min(2, std::atoi(e)));
+    if (const char* e = experiment_env("TCFFT_ABUFS")) p.a_bufs = std::max(1, std::min(2, std::atoi(e)));
   }
   p.smem_b = p.smem_a + p.a_bufs * a_bytes;
   int bsz = ((int)p.bblob.size() * 2 + 127) & ~127;
@@ -612,7 +617,7 @@ bool build_pass(PassPlan& p, int kind, int N, int64_t count, int64_t images, int
   // One CTA per SM: two warpgroups split every stage's tiles (kernel NWG).
   // TCFFT_NWG=<k> (experiment) asks for k warpgroups wherever tiles divide.
   {
-    const char* e = std::getenv("TCFFT_NWG");
+    const char* e = experiment_env("TCFFT_NWG");
     int want = e ? std::atoi(e) : (p.ctas_per_sm == 1 ? 2 : 1);
     while (want > 1) {
       bool div = true;
@@ -644,7 +649,7 @@ bool build_pass(PassPlan& p, int kind, int N, int64_t count, int64_t images, int
 // traffic beat two passes of 16-byte runs (N1 = N2 = 2048) at these sizes.
 static int build_three_step(Plan& plan, int nx, int lg, int64_t batch, std::string* err) {
   int a = lg / 3, b = (lg - a) / 2, c = lg - a - b;
-  if (const char* e = std::getenv("TCFFT_THREE_SPLIT")) {  // experiment hook: "a,b,c" (log2 N1, N2, N3)
+  if (const char* e = experiment_env("TCFFT_THREE_SPLIT")) {  // experiment hook: "a,b,c" (log2 N1, N2, N3)
     int x, y, z;
     if (std::sscanf(e, "%d,%d,%d", &x, &y, &z) == 3 && x + y + z == lg) a = x, b = y, c = z;
   }
@@ -708,7 +713,7 @@ int build_plan(Plan& plan, int dims, int nx, int ny, int64_t batch, std::string*
     }
     // Three passes for N >= 2^19 (every strided access keeps >= 64-byte
     // runs, see below); two passes up to 2^18, whose strips are >= 32 B wide.
-    const char* e3 = std::getenv("TCFFT_THREE_PASS");
+    const char* e3 = experiment_env("TCFFT_THREE_PASS");
     if (lg >= 19 && (!e3 || std::atoi(e3) != 0)) return build_three_step(plan, nx, lg, batch, err);
     const int N1 = 1 << (lg / 2), N2 = 1 << (lg - lg / 2);
     // The batch is walked in L2-sized groups of G transforms (two launches per
@@ -718,7 +723,7 @@ int build_plan(Plan& plan, int dims, int nx, int ny, int64_t batch, std::string*
     // (opt-in: measured slower than one ungrouped launch per pass in round 1,
     // 17.9 vs 18.9 TFLOP/s for C3 at 128 MiB groups with CUDA-graph replay)
     int64_t group_mb = 0;
-    if (const char* e = std::getenv("TCFFT_FOURSTEP_MB")) group_mb = std::max(0, std::atoi(e));
+    if (const char* e = experiment_env("TCFFT_FOURSTEP_MB")) group_mb = std::max(0, std::atoi(e));
     int64_t G = batch;
     if (group_mb > 0) {
       G = std::max<int64_t>(1, (group_mb << 20) / ((int64_t)nx * 4));

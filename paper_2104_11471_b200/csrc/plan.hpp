@@ -126,6 +126,12 @@ struct Plan {
   std::vector<PassPlan> passes;
 };
 
+// Experiment hooks (A/B measurements only, never needed by users): returns
+// getenv(name) when the process sets TCFFT_EXPERIMENTS=1, else nullptr, so a
+// stray environment variable cannot change a plan.  The only getenv calls in
+// the library are inside this gate.
+const char* experiment_env(const char* name);
+
 // Radix list chosen for a single-pass transform of length n (product == n).
 std::vector<int> choose_radices(int n, int kind = kPassRow, bool twiddled = false);
 // row-block interleave of a writer stage of radix R (kernel Cfg::HSTEP mirrors it)

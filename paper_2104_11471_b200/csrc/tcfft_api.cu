@@ -14,7 +14,6 @@
 
 #include "../../include/tcfft_b200.h"
 #include "fft_kernel.cuh"
-#include "fft_fused.cuh"
 #include "plan.hpp"
 
 using tcfft::KParams;
@@ -36,7 +35,7 @@ struct KernelEntry {
 // first TMA touches the data, so stream order is preserved.
 static int pdl_mode() {
   static const int m = [] {
-    const char* e = std::getenv("TCFFT_PDL");
+    const char* e = tcfft::experiment_env("TCFFT_PDL");
     return e ? std::atoi(e) : 1;
   }();
   return m;
@@ -126,58 +125,6 @@ const KernelEntry* find_kernel(const PassPlan& p) {
   return nullptr;
 }
 
-// ---- fused two-pass kernels (2D row + column passes) ------------------------
-struct FusedEntry {
-  int EA, RA1, RA2, RA3, modeA, tw4A;
-  int EB, RB1, RB2, RB3, modeB;
-  int minb;
-  const void* fn;
-  void (*launch)(dim3, int, cudaStream_t, const CUtensorMap&, const CUtensorMap&, const CUtensorMap&,
-                 const CUtensorMap&, const tcfft::FusedParams&);
-};
-
-template <class PA, class PB, int MINB>
-void launch_fused_tpl(dim3 grid, int smem, cudaStream_t st, const CUtensorMap& a0, const CUtensorMap& a1,
-                      const CUtensorMap& b0, const CUtensorMap& b1, const tcfft::FusedParams& f) {
-  tcfft::fft_fused_kernel<PA, PB, MINB><<<grid, 160, smem, st>>>(a0, a1, b0, b1, f);
-}
-
-template <int EA, int A1, int A2, int A3, int MA, bool TWA, int EB, int B1, int B2, int B3, int MB_>
-struct FusedPair {
-  using CA = tcfft::dev::Cfg<EA, A1, A2, A3, MA>;
-  using CB = tcfft::dev::Cfg<EB, B1, B2, B3, MB_>;
-  using FR = tcfft::dev::FusedRec<CA, CB, TWA, false>;
-  using PA = tcfft::dev::PassT<EA, A1, A2, A3, MA, TWA, FR::COL_A>;
-  using PB = tcfft::dev::PassT<EB, B1, B2, B3, MB_, false, FR::COL_B>;
-};
-#define FENTRY(EA, A1, A2, A3, MA, TWA, EB, B1, B2, B3, MB_, MINB)                                         \
-  {                                                                                                      \
-    EA, A1, A2, A3, MA, TWA, EB, B1, B2, B3, MB_, MINB,                                                  \
-        (const void*)&tcfft::fft_fused_kernel<FusedPair<EA, A1, A2, A3, MA, TWA, EB, B1, B2, B3, MB_>::PA,   \
-                                              FusedPair<EA, A1, A2, A3, MA, TWA, EB, B1, B2, B3, MB_>::PB, MINB>, \
-        &launch_fused_tpl<FusedPair<EA, A1, A2, A3, MA, TWA, EB, B1, B2, B3, MB_>::PA,                  \
-                          FusedPair<EA, A1, A2, A3, MA, TWA, EB, B1, B2, B3, MB_>::PB, MINB>             \
-  }
-// 2D square sizes: row pass (mode 0) then column-strip pass (mode 1)
-const FusedEntry kFused[] = {
-    FENTRY(4096, 16, 16, 0, 0, false, 4096, 16, 16, 0, 1, 4),   // 256^2
-    FENTRY(4096, 16, 32, 0, 0, false, 4096, 16, 32, 0, 1, 4),   // 512^2
-    FENTRY(4096, 32, 32, 0, 0, false, 4096, 32, 32, 0, 1, 4),   // 1024^2
-    FENTRY(4096, 16, 16, 8, 0, false, 8192, 16, 16, 8, 1, 2),   // 2048^2
-};
-
-const FusedEntry* find_fused(const PassPlan& a, const PassPlan& b) {
-  int ra[3] = {0, 0, 0}, rb[3] = {0, 0, 0};
-  for (int s = 0; s < a.S; ++s) ra[s] = a.st[s].R;
-  for (int s = 0; s < b.S; ++s) rb[s] = b.st[s].R;
-  const int tw = a.tw4_total ? 1 : 0;
-  for (const auto& k : kFused)
-    if (k.EA == a.E && k.RA1 == ra[0] && k.RA2 == ra[1] && k.RA3 == ra[2] && k.modeA == a.kind && k.tw4A == tw &&
-        k.EB == b.E && k.RB1 == rb[0] && k.RB2 == rb[1] && k.RB3 == rb[2] && k.modeB == b.kind)
-      return &k;
-  return nullptr;
-}
-
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   static std::once_flag once;
@@ -209,18 +156,9 @@ struct DevPass {
 
 struct HostPipe;
 
-struct FusedState {
-  const FusedEntry* k = nullptr;
-  tcfft::FusedParams f{};
-  int smem = 0, grid = 0;
-  int32_t* counters = nullptr;
-  bool dynamic = true;
-};
-
 struct tcfftPlanImpl {
   tcfft::Plan plan;
   std::vector<DevPass> dev;
-  FusedState fused;
   void* ws = nullptr;
   HostPipe* pipe = nullptr;  // lazily built by tcfftExecC2CHost
   unsigned pass_mask = ~0u;  // tcfftSetPassMask (profiling)
@@ -331,82 +269,29 @@ tcfftResult map_build_status(int st) {
   }
 }
 
-// Fused single-launch execution of a two-pass plan (2D): rows then columns of
-// L2-sized image groups, see fft_fused.cuh.  Silently skipped when the
-// geometry or the kernel instantiation does not fit (two launches are used).
-void build_fused(tcfftPlanImpl* h, const cudaDeviceProp& prop) {
-  // Opt-in (TCFFT_FUSED=1): halves the HBM traffic of 2D plans (measured 2.24 vs
-  // 4.2 GB for 512x512x1024) but the single-launch schedule is not faster yet
-  // (0.88 ms vs 0.77 ms with two pipelined launches, round 1).
-  const char* e = std::getenv("TCFFT_FUSED");
-  if (!e || std::atoi(e) == 0) return;
-  if (h->plan.passes.size() != 2 || h->plan.dims != 2) return;
-  const PassPlan& A = h->plan.passes[0];
-  const PassPlan& B = h->plan.passes[1];
-  if (B.IMG != 1 || (B.in.mode != tcfft::kIoBox && B.in.mode != tcfft::kIoBoxR)) return;  // column strips of one image per chunk
-  const int64_t objs = h->plan.batch;
-  const int64_t rows_per_obj = h->plan.nx;             // pass A: rows of length ny
-  if (rows_per_obj % A.T) return;
-  const int a_per_obj = (int)(rows_per_obj / A.T);
-  const int b_per_obj = B.in.spi;
-  const FusedEntry* k = find_fused(A, B);
-  if (!k) return;
-  // group: ~16 MiB of data per group, objects per group dividing the batch
-  const int64_t obj_bytes = (int64_t)h->plan.nx * h->plan.ny * 4;
-  int64_t group_mb = 16;
-  if (const char* g = std::getenv("TCFFT_FUSED_MB")) group_mb = std::max(1, std::atoi(g));
-  int64_t opg = std::max<int64_t>(1, (group_mb << 20) / obj_bytes);
-  while (opg > 1 && objs % opg) --opg;
-  const int64_t groups = objs / opg;
-  int lag = 1;
-  if (const char* l = std::getenv("TCFFT_FUSED_LAG")) lag = std::max(1, std::atoi(l));
-  if (groups <= lag) return;  // too small to pipeline groups: two launches are as good
-  // shared-memory layout covering both passes
-  auto al = [](int x, int a) { return (x + a - 1) / a * a; };
-  const int stage = std::max(A.smem_a, B.smem_a);
-  const int abytes = std::max(A.a_bytes, B.a_bytes);
-  const int bA = al((int)A.bblob.size() * 2, 128), bB = al((int)B.bblob.size() * 2, 128);
-  const int smem_a = stage, smem_ba = smem_a + abytes, smem_bb = smem_ba + bA, smem_tw4 = smem_bb + bB;
-  const int tw4 = A.smem_bar - A.smem_tw4;
-  const int smem_bar = smem_tw4 + tw4;
-  const int smem = smem_bar + 128 + 1024;  // 5 mbarriers, TMEM address, item ring + alignment slack
-  const int tmem_cols = std::max(A.tmem_cols, B.tmem_cols);
-  const int ctas = std::max(1, std::min(std::min(512 / tmem_cols, 233472 / (smem + 1024)), k->minb));
-  FusedState& F = h->fused;
-  if (cudaMalloc(&F.counters, objs * sizeof(int32_t) + 16) != cudaSuccess) {
-    cudaGetLastError();
-    F.counters = nullptr;
-    return;
+void destroy_pipe_fwd(HostPipe* hp);
+
+// Frees everything a (possibly partially built) plan owns; shared by
+// tcfftDestroy and every failure path of create().
+void release(tcfftPlanImpl* h) {
+  for (auto& q : h->dev) {
+    if (q.tables) cudaFree(q.tables);
+#ifdef TCFFT_TRACE
+    if (q.kp.trace) cudaFree(q.kp.trace);
+#endif
   }
-  F.k = k;
-  F.smem = smem;
-  tcfft::FusedParams& f = F.f;
-  f.a = h->dev[0].kp;
-  f.b = h->dev[1].kp;
-  for (KParams* kp : {&f.a, &f.b}) {
-    kp->smem_a = smem_a;
-    kp->a_stride = 0;
-    kp->smem_bar = smem_bar;
-    kp->smem_tw4 = smem_tw4;
-  }
-  f.a.smem_b = smem_ba;
-  f.b.smem_b = smem_bb;
-  f.smem_a_b = smem_bb;
-  f.groups = groups;
-  f.lag = lag;
-  f.objs_per_group = (int)opg;
-  f.a_per_obj = a_per_obj;
-  f.b_per_obj = b_per_obj;
-  f.objs = objs;
-  f.items = groups * opg * (int64_t)(a_per_obj + b_per_obj);
-  f.counters = F.counters;
-  f.epoch_base = 0;
-  F.dynamic = !(std::getenv("TCFFT_FUSED_STATIC") && std::atoi(std::getenv("TCFFT_FUSED_STATIC")));
-  f.next_item = F.dynamic ? reinterpret_cast<unsigned long long*>(
-                                reinterpret_cast<char*>(F.counters) + ((objs * sizeof(int32_t) + 7) & ~size_t(7)))
-                          : nullptr;
-  cudaFuncSetAttribute(k->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)prop.sharedMemPerBlockOptin);
-  F.grid = (int)std::min<int64_t>(f.items, (int64_t)prop.multiProcessorCount * ctas);
+  h->dev.clear();
+  if (h->ws) cudaFree(h->ws);
+  if (h->scratch) cudaFree(h->scratch);
+  for (auto& e : h->graphs) cudaGraphExecDestroy(e.exec);
+  h->graphs.clear();
+  if (h->cap_stream) cudaStreamDestroy(h->cap_stream);
+  destroy_pipe_fwd(h->pipe);
+  h->ws = h->scratch = nullptr;
+  h->cap_stream = nullptr;
+  h->pipe = nullptr;
+  h->magic = 0;
+  delete h;
 }
 
 tcfftResult create(tcfftHandle* out, int dims, int nx, int ny, int batch) {
@@ -437,7 +322,7 @@ tcfftResult create(tcfftHandle* out, int dims, int nx, int ny, int batch) {
     DevPass d;
     d.k = find_kernel(p);
     if (!d.k) {
-      delete h;
+      release(h);
       return TCFFT_NOT_SUPPORTED;
     }
     size_t rb = p.rows_tab.size() * sizeof(tcfft::RowInfo);
@@ -446,8 +331,7 @@ tcfftResult create(tcfftHandle* out, int dims, int nx, int ny, int batch) {
     size_t rb_al = (rb + 255) & ~size_t(255);
     if (cudaMalloc(&d.tables, rb_al + bb + tb + 256 + kTicketSlots * 16) != cudaSuccess) {
       cudaGetLastError();
-      for (auto& q : h->dev) cudaFree(q.tables);
-      delete h;
+      release(h);
       return TCFFT_ALLOC_FAILED;
     }
     char* base = static_cast<char*>(d.tables);
@@ -480,7 +364,7 @@ tcfftResult create(tcfftHandle* out, int dims, int nx, int ny, int batch) {
     // gather-ahead shifts when each CTA's stores land; the four-step passes
     // write 16-byte runs whose L2 merging is timing sensitive: keep them lockstep
     k.gather_ahead = (p.tw4_total || p.kind == tcfft::kPassRowT) ? 0 : 1;
-    if (const char* e = std::getenv("TCFFT_GATHER_AHEAD")) k.gather_ahead = std::atoi(e);
+    if (const char* e = tcfft::experiment_env("TCFFT_GATHER_AHEAD")) k.gather_ahead = std::atoi(e);
     // pipelined loop: measured faster only for the N = 1024 (32, 32) row pass
     // (0.92 vs 0.88 of roofline); slower for the 512 row pass (0.88 vs 0.97),
     // every column strip (2D 2048^2: 0.48 vs 0.60) and the twiddled passes
@@ -495,7 +379,7 @@ tcfftResult create(tcfftHandle* out, int dims, int nx, int ny, int batch) {
     // rounds stay static: the ticket + retire atomics cost short kernels (C1).
     // TCFFT_DYNAMIC=0: static; 1: tickets for every chunk after the first.
     const int dyn_mode = [] {
-      const char* e = std::getenv("TCFFT_DYNAMIC");
+      const char* e = tcfft::experiment_env("TCFFT_DYNAMIC");
       return e ? std::atoi(e) : 2;
     }();
     const int64_t slots0 = (int64_t)prop.multiProcessorCount * p.ctas_per_sm;
@@ -507,9 +391,9 @@ tcfftResult create(tcfftHandle* out, int dims, int nx, int ny, int batch) {
       k.ctr = reinterpret_cast<unsigned long long*>(base + rb_al + bb + tb + 256);
       cudaMemset(k.ctr, 0, kTicketSlots * 2 * sizeof(unsigned long long));
     }
-    if (const char* e = std::getenv("TCFFT_PDL_MASK"))
+    if (const char* e = tcfft::experiment_env("TCFFT_PDL_MASK"))
       if (!((std::atoi(e) >> h->dev.size()) & 1)) k.pdl = 0;
-    if (const char* e = std::getenv("TCFFT_PIPE")) k.pipe = std::atoi(e) && p.S >= 2 && p.kind != tcfft::kPassRowT;
+    if (const char* e = tcfft::experiment_env("TCFFT_PIPE")) k.pipe = std::atoi(e) && p.S >= 2 && p.kind != tcfft::kPassRowT;
     // the opt-in maximum: one kernel instance serves plans with different
     // shared-memory requests, occupancy follows each launch's own request
     cudaFuncSetAttribute(d.k->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)prop.sharedMemPerBlockOptin);
@@ -518,7 +402,7 @@ tcfftResult create(tcfftHandle* out, int dims, int nx, int ny, int batch) {
     k.static_chunks = d.grid;
     if (k.ctr && dyn_mode == 2) {
       static const int tail = [] {  // ticketed rounds at the end (experiment hook TCFFT_DYN_TAIL)
-        const char* e = std::getenv("TCFFT_DYN_TAIL");
+        const char* e = tcfft::experiment_env("TCFFT_DYN_TAIL");
         return e ? std::max(1, std::atoi(e)) : 2;
       }();
       k.static_chunks = std::max<int64_t>(d.grid, (p.chunks / d.grid - tail) * d.grid);
@@ -528,17 +412,13 @@ tcfftResult create(tcfftHandle* out, int dims, int nx, int ny, int batch) {
 #endif
     h->dev.push_back(d);
   }
-  build_fused(h, prop);
   if (h->plan.ws_bytes && cudaMalloc(&h->ws, h->plan.ws_bytes) != cudaSuccess) {
     cudaGetLastError();
-    for (auto& q : h->dev) cudaFree(q.tables);
-    delete h;
+    release(h);
     return TCFFT_ALLOC_FAILED;
   }
   if (cudaGetLastError() != cudaSuccess) {
-    for (auto& q : h->dev) cudaFree(q.tables);
-    if (h->ws) cudaFree(h->ws);
-    delete h;
+    release(h);
     return TCFFT_EXEC_FAILED;
   }
   *out = h;
@@ -546,6 +426,18 @@ tcfftResult create(tcfftHandle* out, int dims, int nx, int ny, int batch) {
 }
 
 bool valid(tcfftHandle h) { return h && h->magic == 0x7cff7; }
+
+// The plan's tables, tensor maps and workspace live on the device that was
+// current at plan creation: executing with another current device would read
+// another GPU's memory (or fail at launch), so it is refused.
+bool on_plan_device(tcfftHandle h) {
+  int cur = -1;
+  if (cudaGetDevice(&cur) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return cur == h->device;
+}
 
 }  // namespace
 
@@ -578,24 +470,8 @@ tcfftResult tcfftSetPassMask(tcfftHandle plan, unsigned mask) {
 
 tcfftResult tcfftExecC2C(tcfftHandle plan, const void* idata, void* odata) {
   if (!valid(plan)) return TCFFT_INVALID_PLAN;
-  if (!idata || !odata) return TCFFT_INVALID_VALUE;
+  if (!idata || !odata || !on_plan_device(plan)) return TCFFT_INVALID_VALUE;
   if ((reinterpret_cast<uintptr_t>(idata) | reinterpret_cast<uintptr_t>(odata)) & 15) return TCFFT_INVALID_VALUE;
-  if (plan->fused.k && plan->pass_mask == ~0u) {
-    const PassPlan& A = plan->plan.passes[0];
-    const PassPlan& B = plan->plan.passes[1];
-    CUtensorMap a0, a1, b0, b1;
-    if (make_tmap(&a0, A.in, idata) != TCFFT_SUCCESS || make_tmap(&a1, A.out, odata) != TCFFT_SUCCESS ||
-        make_tmap(&b0, B.in, odata) != TCFFT_SUCCESS || make_tmap(&b1, B.out, odata) != TCFFT_SUCCESS)
-      return TCFFT_EXEC_FAILED;
-    tcfft::FusedParams f = plan->fused.f;
-    f.a.in.gptr = static_cast<const uint8_t*>(idata);
-    f.a.out.gptr = static_cast<const uint8_t*>(odata);
-    f.b.in.gptr = static_cast<const uint8_t*>(odata);
-    f.b.out.gptr = static_cast<const uint8_t*>(odata);
-    cudaMemsetAsync(plan->fused.counters, 0, (size_t)f.objs * sizeof(int32_t) + 16, plan->stream);
-    plan->fused.k->launch(dim3(plan->fused.grid), plan->fused.smem, plan->stream, a0, a1, b0, b1, f);
-    return cudaGetLastError() == cudaSuccess ? TCFFT_SUCCESS : TCFFT_EXEC_FAILED;
-  }
   if (plan->plan.groups > 1 && plan->pass_mask == ~0u) return exec_grouped(plan, idata, odata);
   return launch_passes(plan, idata, odata, plan->stream);
 }
@@ -668,7 +544,6 @@ static tcfftResult exec_grouped(tcfftHandle plan, const void* idata, void* odata
   return cudaGraphLaunch(ex, plan->stream) == cudaSuccess ? TCFFT_SUCCESS : TCFFT_EXEC_FAILED;
 }
 
-extern "C" {
 
 // ---------------------------------------------------------------------------
 // Host-buffer execution: the batch is cut into slices of whole transforms;
@@ -683,6 +558,11 @@ struct HostPipe {
   cudaEvent_t ev_in[3], ev_done[3], ev_free[3], ev_start, ev_end;
   bool ok = false;
 };
+
+static void destroy_pipe(HostPipe* hp);
+namespace {
+void destroy_pipe_fwd(HostPipe* hp) { destroy_pipe(hp); }
+}  // namespace
 
 static void destroy_pipe(HostPipe* hp) {
   if (!hp) return;
@@ -711,7 +591,7 @@ static tcfftResult build_pipe(tcfftHandle plan) {
   auto* hp = new (std::nothrow) HostPipe();
   if (!hp) return TCFFT_ALLOC_FAILED;
   int64_t target = 16ll << 20;  // ~16 MiB slices (measured best of 8..128 MiB for C2)
-  if (const char* e = std::getenv("TCFFT_SLICE_MB")) target = std::max(1, std::atoi(e)) * (1ll << 20);
+  if (const char* e = tcfft::experiment_env("TCFFT_SLICE_MB")) target = std::max(1, std::atoi(e)) * (1ll << 20);
   hp->slice_batch = std::max<int64_t>(1, std::min<int64_t>(P.batch, target / bytes_per));
   hp->slices = (P.batch + hp->slice_batch - 1) / hp->slice_batch;
   hp->tail = P.batch - (hp->slices - 1) * hp->slice_batch;
@@ -744,7 +624,7 @@ static tcfftResult build_pipe(tcfftHandle plan) {
 
 extern "C" tcfftResult tcfftExecC2CHost(tcfftHandle plan, const void* hin, void* hout) {
   if (!valid(plan)) return TCFFT_INVALID_PLAN;
-  if (!hin || !hout) return TCFFT_INVALID_VALUE;
+  if (!hin || !hout || !on_plan_device(plan)) return TCFFT_INVALID_VALUE;
   if (!plan->pipe) {
     tcfftResult st = build_pipe(plan);
     if (st != TCFFT_SUCCESS) return st;
@@ -813,6 +693,7 @@ __global__ void strided_copy_kernel(const uint32_t* __restrict__ src, uint32_t* 
 extern "C" tcfftResult tcfftExecC2CStrided(tcfftHandle plan, const void* idata, void* odata, long long stride,
                                            long long batch_stride) {
   if (!valid(plan)) return TCFFT_INVALID_PLAN;
+  if (!idata || !odata || !on_plan_device(plan)) return TCFFT_INVALID_VALUE;
   const tcfft::Plan& P = plan->plan;
   const int64_t n = (int64_t)P.nx * (P.dims == 2 ? P.ny : 1);
   if (stride < 1 || (P.batch > 1 && batch_stride < stride * n) || batch_stride < 1) return TCFFT_INVALID_VALUE;
@@ -838,8 +719,6 @@ extern "C" tcfftResult tcfftExecC2CStrided(tcfftHandle plan, const void* idata, 
   const size_t bytes = (size_t)(P.batch * n * 4);
   if (plan->scratch_bytes < bytes) {
     if (plan->scratch) cudaFree(plan->scratch);
-  for (auto& e : plan->graphs) cudaGraphExecDestroy(e.exec);
-  if (plan->cap_stream) cudaStreamDestroy(plan->cap_stream);
     plan->scratch = nullptr;
     plan->scratch_bytes = 0;
     if (cudaMalloc(&plan->scratch, bytes) != cudaSuccess) {
@@ -873,17 +752,11 @@ extern "C" int tcfftDebugTrace(tcfftHandle plan, int i, void* host, size_t n) {
 }
 #endif
 
+extern "C" {
+
 tcfftResult tcfftDestroy(tcfftHandle plan) {
   if (!valid(plan)) return TCFFT_INVALID_PLAN;
-  for (auto& q : plan->dev) cudaFree(q.tables);
-  if (plan->ws) cudaFree(plan->ws);
-  if (plan->fused.counters) cudaFree(plan->fused.counters);
-  if (plan->scratch) cudaFree(plan->scratch);
-  for (auto& e : plan->graphs) cudaGraphExecDestroy(e.exec);
-  if (plan->cap_stream) cudaStreamDestroy(plan->cap_stream);
-  destroy_pipe(plan->pipe);
-  plan->magic = 0;
-  delete plan;
+  release(plan);
   return TCFFT_SUCCESS;
 }
 

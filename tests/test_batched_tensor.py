@@ -5,6 +5,7 @@ import numpy as np
 import pytest
 
 from oracle import restate as R
+from tests._parity import gates
 
 torch = pytest.importorskip("torch")
 import paper_2104_11471_b200 as tc  # noqa: E402
@@ -59,6 +60,7 @@ def test_strided_views_equal_contiguous(n, batch, stride, bstride):
     tc.execute(tc.plan_1d(n, batch), y)
     want = y.cpu().numpy()
     assert np.array_equal(got[idx].view(np.uint16), want.view(np.uint16))
+    gates(got[idx], x, n)  # and against the reference restatement (oracle)
     mask = np.ones(len(buf), bool)
     mask[idx.reshape(-1)] = False
     assert np.all(got[mask] == np.float16(7.0))  # nothing outside the view touched
