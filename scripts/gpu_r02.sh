@@ -18,6 +18,6 @@ if [[ $WHAT == all || $WHAT == bench ]]; then
   cat $OUT/bench_$TAG.json; tail -5 $OUT/bench_$TAG.err
 fi
 if [[ $WHAT == all || $WHAT == ref ]]; then
-  /usr/bin/time -v timeout 1200 python bench.py --impl reference --steps 20 --warmup 5 > $OUT/bench_ref_$TAG.json 2> $OUT/bench_ref_$TAG.err
-  cat $OUT/bench_ref_$TAG.json; grep -E "Elapsed|Maximum resident" $OUT/bench_ref_$TAG.err
+  ( time timeout 1200 python bench.py --impl reference --steps 20 --warmup 5 ) > $OUT/bench_ref_$TAG.json 2> $OUT/bench_ref_$TAG.err
+  cat $OUT/bench_ref_$TAG.json; tail -4 $OUT/bench_ref_$TAG.err
 fi
