@@ -255,6 +255,11 @@ bool build_pass(PassPlan& p, int kind, int N, int64_t count, int64_t images, int
     // rows of an images x (count/images) x N array, output transposed into
     // images x N x (count/images): >= 4 rows per chunk (>= 16 B output runs)
     p.E = std::max(chunk_elems_for(N), 4 * N);
+    {
+      char key[32];  // experiment hook: TCFFT_RCHUNK_<n>=<elems> overrides the transposed-row chunk size
+      std::snprintf(key, sizeof(key), "TCFFT_RCHUNK_%d", N);
+      if (const char* e = experiment_env(key)) p.E = std::atoi(e);
+    }
     p.T = p.E / N;
     p.count = count;
     p.chunks = (count + p.T - 1) / p.T;

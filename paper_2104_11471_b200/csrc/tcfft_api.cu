@@ -98,6 +98,9 @@ const KernelEntry kKernels[] = {
     // one-CTA-per-SM passes with two warpgroups (plan.cpp PassPlan::nwg)
     KENTRYW(16384, 16, 32, 32, 1, 0, false, 2), KENTRYW(16384, 64, 64, 0, 1, 1, false, 2),
     KENTRYW(16384, 64, 32, 0, 1, 1, false, 2),
+    // two-pass four-step 2^22 with 32-byte runs (experiment: TCFFT_THREE_PASS=0,
+    // TCFFT_SCHUNK_2048 / TCFFT_RCHUNK_2048 = 16384)
+    KENTRYW(16384, 64, 32, 0, 1, 1, true, 2), KENTRYW(16384, 64, 32, 0, 1, 2, false, 2),
     // column strips of 256 columns for N <= 8 (2D nx <= 8 with ny > 256)
     KSTRIP(512, 2, 0, 0, 4),      KSTRIP(1024, 4, 0, 0, 4),     KSTRIP(2048, 8, 0, 0, 4),
     // rows of 4 .. 16 whose element count is not a multiple of 32 (unswizzled staging)
@@ -178,6 +181,19 @@ struct tcfftPlanImpl {
 
 namespace {
 
+// L2 sector promotion of the strided (column-box) tensor maps: a box row of
+// C*4 bytes fetches only its own sectors (NONE) or the whole 64/128/256-byte
+// line, which the CTA working on the neighbouring strip then hits in L2
+// (experiment hook TCFFT_L2PROMO = 0 / 64 / 128 / 256).
+CUtensorMapL2promotion box_promotion() {
+  const char* e = tcfft::experiment_env("TCFFT_L2PROMO");
+  const int v = e ? std::atoi(e) : 0;
+  return v == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+         : v == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+         : v == 256 ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B
+                    : CU_TENSOR_MAP_L2_PROMOTION_NONE;
+}
+
 tcfftResult make_tmap(CUtensorMap* tm, const tcfft::IoDesc& io, const void* base) {
   std::memset(tm, 0, sizeof(*tm));
   if (io.mode == tcfft::kIoPitch) return TCFFT_SUCCESS;  // raw bulk copies, no tensor map
@@ -221,7 +237,7 @@ tcfftResult make_tmap(CUtensorMap* tm, const tcfft::IoDesc& io, const void* base
                             : run == 32 ? CU_TENSOR_MAP_SWIZZLE_32B
                                         : CU_TENSOR_MAP_SWIZZLE_NONE;
     r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, const_cast<void*>(base), dims, strides, box, es,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            CU_TENSOR_MAP_INTERLEAVE_NONE, sw, box_promotion(), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   } else {
     const int64_t rs = io.row_stride ? io.row_stride : io.cols;
     const int64_t is = io.img_stride ? io.img_stride : (int64_t)io.cols * io.rows;
@@ -238,7 +254,7 @@ tcfftResult make_tmap(CUtensorMap* tm, const tcfft::IoDesc& io, const void* base
                             : run == 32 ? CU_TENSOR_MAP_SWIZZLE_32B
                                         : CU_TENSOR_MAP_SWIZZLE_NONE;
     r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_UINT32, rank, const_cast<void*>(base), dims, strides, box, es,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            CU_TENSOR_MAP_INTERLEAVE_NONE, sw, box_promotion(), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   }
   return r == CUDA_SUCCESS ? TCFFT_SUCCESS : TCFFT_EXEC_FAILED;
 }

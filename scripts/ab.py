@@ -13,12 +13,12 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def run(cfg, env, steps):
-    e = dict(os.environ)
+    e = dict(os.environ, TCFFT_EXPERIMENTS="1")
     for kv in env.split():
         k, v = kv.split("=", 1)
         e[k] = v
     out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--config", cfg, "--steps", str(steps),
-                          "--warmup", "5", "--no-cpu", "--no-e2e"], capture_output=True, text=True, env=e, cwd=ROOT)
+                          "--warmup", "5", "--no-cpu", "--no-e2e", "--no-nested"], capture_output=True, text=True, env=e, cwd=ROOT)
     try:
         d = json.loads(out.stdout.strip().splitlines()[-1])
         return d["value"], d["ms_per_step"]
