@@ -427,18 +427,20 @@ DEVI void issue_store(const CUtensorMap* tm, const KIo& io, int T, int64_t chunk
   bulk_commit();
 }
 
-// Issue the MMAs of stage s (one elected thread).
-template <class C, int s>
+// Issue the MMAs of stage s (one elected thread).  Stage 0 may be issued for
+// a tile range [TB, TE) whose accumulators start at TMEM column (t - TB) * NP
+// (single-buffer passes run stage 0 in two halves sharing one D region).
+template <class C, int s, int TB = 0, int TE = C::T(s), bool DSHIFT = false>
 DEVI void issue_stage_mma(uint32_t s_a, uint32_t s_b, uint32_t tD, uint32_t tA) {
   constexpr int KP = C::KP(s), NP = C::NP(s), T = C::T(s);
   if constexpr (s == 0) {
     constexpr uint32_t idesc = make_idesc_f16(128, NP, 0, 0);  // A (TMEM) K-major, B K-major
 #pragma unroll
-    for (int t = 0; t < T; ++t)
+    for (int t = TB; t < TE; ++t)
 #pragma unroll
       for (int q = 0; q < KP / 16; ++q)
-        mma_ts(tD + t * NP, tA + t * (KP / 2) + q * 8, make_sdesc(s_b + C::BOFF(s) + q * 32 * NP, 128, 256), idesc,
-               q > 0);
+        mma_ts(tD + (DSHIFT ? t - TB : t) * NP, tA + t * (KP / 2) + q * 8,
+               make_sdesc(s_b + C::BOFF(s) + q * 32 * NP, 128, 256), idesc, q > 0);
   } else {
     constexpr uint32_t idesc = make_idesc_f16(128, NP, 1, 0);  // A MN-major (split planes), B K-major
 #pragma unroll
@@ -456,7 +458,15 @@ DEVI void issue_stage_mma(uint32_t s_a, uint32_t s_b, uint32_t tD, uint32_t tA) 
 // of every stage (TMEM lane quarter = warp % 4).  Two warpgroups for the
 // one-CTA-per-SM passes (E = 16384), whose chunk loop is otherwise latency
 // bound on a single warp per SM sub-partition.
-template <int E, int R1, int R2, int R3, int MINB, int MODE, bool TW4, int NWG = 1>
+// ONEBUF: single-buffer passes (chunks of 16384 elements, two CTAs per SM).
+// One shared-memory buffer holds a chunk for its whole life: TMA load ->
+// stage-1 gather (to TMEM) -> every later stage's A operand -> output staging
+// -> TMA store; the next chunk's load is issued once the store has read the
+// buffer, while the SM's other CTA computes.  Stage 1 runs in two halves of
+// tiles sharing one accumulator region, so a CTA needs 256 TMEM columns
+// (D/2 + the stage-1 A operand, then the full D of later stages over the dead
+// A operand) and two CTAs fit an SM.
+template <int E, int R1, int R2, int R3, int MINB, int MODE, bool TW4, int NWG = 1, bool ONEBUF = false>
 __global__ void __launch_bounds__(128 * NWG, MINB)
     fft_pass_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ CUtensorMap tm_out,
                     const KParams p) {
@@ -464,10 +474,15 @@ __global__ void __launch_bounds__(128 * NWG, MINB)
   using C = Cfg<E, R1, R2, R3, MODE>;
   constexpr int S = C::S;
   constexpr int TM = C::TMAX;
+  constexpr int T0 = C::T(0);
+  constexpr int DH = T0 / 2 * C::NP(0);  // ONEBUF: stage-1 accumulator columns per half
+  static_assert(!ONEBUF || (NWG == 1 && T0 % 2 == 0 && S >= 2 && DH + C::ACOLS <= 256 && C::DCOLS <= 256),
+                "single-buffer geometry");
+  constexpr uint32_t TCOLS = ONEBUF ? 256u : C::COLS;
   // Transposed-row passes write 16-byte runs whose merging in L2 is sensitive
   // to store timing: they keep the simple (lock-step) chunk loop, measured 1.6x
   // faster for them than the pipelined loop below (round 1).
-  constexpr bool PIPE_OK = MODE != kModeRowT && S >= 2 && NWG == 1;
+  constexpr bool PIPE_OK = MODE != kModeRowT && S >= 2 && NWG == 1 && !ONEBUF;
   constexpr int NT = 128 * NWG;
   static_assert(C::T(0) % NWG == 0 && C::T(S - 1) % NWG == 0 && C::T(S > 1 ? 1 : 0) % NWG == 0, "NWG tiles");
   const bool PIPE = PIPE_OK && p.pipe;
@@ -505,7 +520,7 @@ __global__ void __launch_bounds__(128 * NWG, MINB)
   // PDL trigger: at CTA start (pdl == 2), else as the CTA takes its last chunk
   if (p.pdl == 2 || (int64_t)blockIdx.x + gridDim.x >= p.chunks) griddep_launch_dependents();
   bool triggered = p.pdl == 2 || (int64_t)blockIdx.x + gridDim.x >= p.chunks;
-  if (warp == 0) tmem_alloc<C::COLS>(s_tmem);
+  if (warp == 0) tmem_alloc<TCOLS>(s_tmem);
   if (tid == 0) {
     mbar_init(&bars[0], 1);
     // tcgen05.commit (+ thread 0's arrive when pipelined; a second arrival in
@@ -531,7 +546,7 @@ __global__ void __launch_bounds__(128 * NWG, MINB)
   auto rec = [&](int s, int t) -> const RowInfo& { return p.rows_tab[((size_t)s * p.tiles_max + t) * 128 + ltid]; };
   // stage-0 writers have c = 1; the final stage needs only its output address
   using RC = Rec<C, TW4>;
-  constexpr bool RT = RC::IN_TMEM && NWG == 1;
+  constexpr bool RT = RC::IN_TMEM && NWG == 1 && !ONEBUF;
   constexpr int TMW = TM / NWG;
   // this thread's tiles: t = wg + NWG * tt
   int gb[TL0];
@@ -560,7 +575,7 @@ __global__ void __launch_bounds__(128 * NWG, MINB)
   const uint32_t tbase = *s_tmem;
   const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
   const uint32_t tD = tbase;
-  const uint32_t tA = tbase + (uint32_t)C::DCOLS;
+  const uint32_t tA = tbase + (uint32_t)(ONEBUF ? DH : C::DCOLS);
   const uint32_t tR = tbase + (uint32_t)RC::COL + lane_off;  // this lane's row records
   if constexpr (RT) {
     uint32_t w[RC::N];
@@ -616,6 +631,9 @@ __global__ void __launch_bounds__(128 * NWG, MINB)
     while (chunk < p.chunks) {
       mbar_wait(&bars[0], ld_phase);
       ld_phase ^= 1;
+      // (single-buffer passes: the gather's TMEM stores reuse columns the
+      // previous chunk's final epilogue read before the last barrier)
+      if constexpr (ONEBUF) tc_fence_after();
 #ifdef TCFFT_TRACE
       if (first && tid == 0 && p.trace) p.trace[blockIdx.x * 8 + 4] = globaltimer_ns();
 #endif
@@ -639,17 +657,22 @@ __global__ void __launch_bounds__(128 * NWG, MINB)
         const int64_t nxt = p.ctr ? s_q[1] : chunk + gridDim.x;
         s_q[0] = nxt;  // read by all threads after this iteration's last barrier
         if (nxt < p.chunks) {
-          issue_load(&tm_in, p.in, p.T, nxt, s_in, &bars[0]);  // staging buffer is free again
+          // (single-buffer passes: issued after this chunk's store, below)
+          if constexpr (!ONEBUF) issue_load(&tm_in, p.in, p.T, nxt, s_in, &bars[0]);  // staging buffer is free again
           if (p.ctr) s_q[1] = next_chunk(nxt);
         } else if (p.pdl == 1 && !triggered) {
           griddep_launch_dependents();  // this CTA's last chunk
         }
-        // the output store that last read this chunk's A buffer is done with it
-        if (p.a_stride)
-          bulk_wait_read1();
-        else
-          bulk_wait_read0();
-        issue_stage_mma<C, 0>(s_a_u, s_b_u, tD, tA);
+        if constexpr (ONEBUF) {
+          issue_stage_mma<C, 0, 0, T0 / 2, true>(s_a_u, s_b_u, tD, tA);  // first half of stage 1
+        } else {
+          // the output store that last read this chunk's A buffer is done with it
+          if (p.a_stride)
+            bulk_wait_read1();
+          else
+            bulk_wait_read0();
+          issue_stage_mma<C, 0>(s_a_u, s_b_u, tD, tA);
+        }
         mma_commit(&bars[1]);
       }
       if constexpr (TW4) {
@@ -709,7 +732,41 @@ __global__ void __launch_bounds__(128 * NWG, MINB)
         mma_phase ^= 1;
         tc_fence_after();
       };
-      if constexpr (S >= 2) writer(std::integral_constant<int, 0>{});
+      if constexpr (ONEBUF) {
+        // stage-1 writer in two halves over one accumulator region: half 0's
+        // epilogue drains D, then the second half of stage 1 refills it
+#pragma unroll
+        for (int tt = 0; tt < T0 / 2; ++tt)
+          writer_epilogue<C, 0>(tD + lane_off + tt * C::NP(0), s_a_u + waddr[0][tt], make_float2(1.f, 0.f),
+                                ww[0][tt]);
+        tc_fence_before();
+        __syncthreads();
+        if (tid == 0) {
+          tc_fence_after();
+          issue_stage_mma<C, 0, T0 / 2, T0, true>(s_a_u, s_b_u, tD, tA);
+          mma_commit(&bars[1]);
+        }
+        mbar_wait(&bars[1], mma_phase);
+        mma_phase ^= 1;
+        tc_fence_after();
+#pragma unroll
+        for (int tt = T0 / 2; tt < T0; ++tt)
+          writer_epilogue<C, 0>(tD + lane_off + (tt - T0 / 2) * C::NP(0), s_a_u + waddr[0][tt],
+                                make_float2(1.f, 0.f), ww[0][tt]);
+        fence_proxy_async_smem();
+        tc_fence_before();
+        __syncthreads();
+        if (tid == 0) {
+          tc_fence_after();
+          issue_stage_mma<C, 1>(s_a_u, s_b_u, tD, tA);
+          mma_commit(&bars[1]);
+        }
+        mbar_wait(&bars[1], mma_phase);
+        mma_phase ^= 1;
+        tc_fence_after();
+      } else if constexpr (S >= 2) {
+        writer(std::integral_constant<int, 0>{});
+      }
       if constexpr (S >= 3) writer(std::integral_constant<int, 1>{});
       [[maybe_unused]] uint32_t rf[C::T(S - 1) * RC::FW];
       if constexpr (RT) {
@@ -747,7 +804,16 @@ __global__ void __launch_bounds__(128 * NWG, MINB)
       fence_proxy_async_smem();
       tc_fence_before();
       __syncthreads();
-      if (tid == 0) issue_store<MODE == kModeStrip4>(&tm_out, p.out, p.T, chunk, s_a);
+      if (tid == 0) {
+        issue_store<MODE == kModeStrip4>(&tm_out, p.out, p.T, chunk, s_a);
+        if constexpr (ONEBUF) {
+          // the buffer is free once the store has read it: load the next chunk
+          if (s_q[0] < p.chunks) {
+            bulk_wait_read0();
+            issue_load(&tm_in, p.in, p.T, s_q[0], s_in, &bars[0]);
+          }
+        }
+      }
 #ifdef TCFFT_TRACE
       if (first && tid == 0 && p.trace) p.trace[blockIdx.x * 8 + 6] = globaltimer_ns();
       first = false;
@@ -958,7 +1024,7 @@ __global__ void __launch_bounds__(128 * NWG, MINB)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (warp == 0) tmem_dealloc<C::COLS>(tbase);
+  if (warp == 0) tmem_dealloc<TCOLS>(tbase);
 }
 
 }  // namespace tcfft

@@ -634,6 +634,39 @@ bool build_pass(PassPlan& p, int kind, int N, int64_t count, int64_t images, int
     // registers: 128 per thread at 512 threads per SM
     if (p.nwg > 1) p.ctas_per_sm = std::max(1, std::min(p.ctas_per_sm, 4 / p.nwg));
   }
+  // Single-buffer passes (kernel ONEBUF): when the two-buffer layout leaves one
+  // CTA per SM (chunks of 16384 elements), one buffer per chunk (staging ==
+  // A operand == output staging) and a stage 1 run in two halves of tiles
+  // (256 TMEM columns) fit two CTAs per SM; the SM's second CTA then hides
+  // the load / MMA / barrier latencies the lone CTA exposed (1D 16384: 0.56 of
+  // roofline with one CTA, round 1).  TCFFT_ONEBUF=0 (experiment) disables.
+  {
+    const char* e = experiment_env("TCFFT_ONEBUF");
+    const bool allow = !e || std::atoi(e) != 0;
+    const int dh = p.st[0].tiles / 2 * p.st[0].NP;
+    const int a1 = p.st[0].tiles * (p.st[0].KP / 2);
+    int dmax = 0;
+    for (int s2 = 0; s2 < S; ++s2) dmax = std::max(dmax, p.st[s2].tiles * p.st[s2].NP);
+    const int buf = (std::max(stage_bytes, a_bytes) + 1023) & ~1023;
+    const int ob_bytes = buf + bsz + tw4_bytes + 64 + 1024;
+    if (allow && p.ctas_per_sm == 1 && E == 16384 && S >= 2 && p.st[0].tiles % 2 == 0 && dh + a1 <= 256 &&
+        dmax <= 256 && 2 * (ob_bytes + 1024) <= 233472) {
+      p.onebuf = 1;
+      p.nwg = 1;
+      p.a_bufs = 1;
+      p.smem_in = 0;
+      p.smem_a = 0;
+      p.a_bytes = buf;
+      p.smem_b = buf;
+      p.smem_t = p.smem_b + bsz;
+      p.smem_tw4 = p.smem_t;
+      p.smem_bar = p.smem_tw4 + tw4_bytes;
+      p.smem_bytes = ob_bytes;
+      p.tmem_cols = 256;
+      p.tmem_a_cols = dh;
+      p.ctas_per_sm = 2;
+    }
+  }
   const int pinned = ((233472 / (p.ctas_per_sm + 1) - 1024 + 1) + 127) & ~127;
   if (p.smem_bytes < pinned && p.ctas_per_sm * (pinned + 1024) <= 233472) p.smem_bytes = pinned;
   return true;

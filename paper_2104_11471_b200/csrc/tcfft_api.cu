@@ -24,7 +24,7 @@ namespace {
 using KernelFn = void (*)(CUtensorMap, CUtensorMap, KParams);
 
 struct KernelEntry {
-  int E, R1, R2, R3, mode, tw4, nwg;
+  int E, R1, R2, R3, mode, tw4, nwg, onebuf;
   const void* fn;
   void (*launch)(dim3, int, cudaStream_t, const CUtensorMap&, const CUtensorMap&, const KParams&);
 };
@@ -41,7 +41,7 @@ static int pdl_mode() {
   return m;
 }
 
-template <int E, int R1, int R2, int R3, int MINB, int MODE, bool TW4, int NWG>
+template <int E, int R1, int R2, int R3, int MINB, int MODE, bool TW4, int NWG, bool OB>
 void launch_tpl(dim3 grid, int smem, cudaStream_t st, const CUtensorMap& a, const CUtensorMap& b,
                 const KParams& p) {
   cudaLaunchConfig_t cfg = {};
@@ -54,15 +54,18 @@ void launch_tpl(dim3 grid, int smem, cudaStream_t st, const CUtensorMap& a, cons
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = p.pdl ? 1 : 0;
-  cudaLaunchKernelEx(&cfg, tcfft::fft_pass_kernel<E, R1, R2, R3, MINB, MODE, TW4, NWG>, a, b, p);
+  cudaLaunchKernelEx(&cfg, tcfft::fft_pass_kernel<E, R1, R2, R3, MINB, MODE, TW4, NWG, OB>, a, b, p);
 }
 
-#define KENTRYW(E, R1, R2, R3, MB, MODE, TW, NWG)                                                         \
-  {                                                                                                       \
-    E, R1, R2, R3, MODE, TW, NWG, (const void*)&tcfft::fft_pass_kernel<E, R1, R2, R3, MB, MODE, TW, NWG>, \
-        &launch_tpl<E, R1, R2, R3, MB, MODE, TW, NWG>                                                     \
+#define KENTRYX(E, R1, R2, R3, MB, MODE, TW, NWG, OB)                                                   \
+  {                                                                                                     \
+    E, R1, R2, R3, MODE, TW, NWG, OB, (const void*)&tcfft::fft_pass_kernel<E, R1, R2, R3, MB, MODE, TW, NWG, OB>, \
+        &launch_tpl<E, R1, R2, R3, MB, MODE, TW, NWG, OB>                                               \
   }
+#define KENTRYW(E, R1, R2, R3, MB, MODE, TW, NWG) KENTRYX(E, R1, R2, R3, MB, MODE, TW, NWG, false)
 #define KENTRY(E, R1, R2, R3, MB, MODE, TW) KENTRYW(E, R1, R2, R3, MB, MODE, TW, 1)
+// single-buffer passes, two CTAs per SM (plan.cpp PassPlan::onebuf)
+#define KONE(E, R1, R2, R3, MODE, TW) KENTRYX(E, R1, R2, R3, 2, MODE, TW, 1, true)
 #define KROW(E, R1, R2, R3, MB) KENTRY(E, R1, R2, R3, MB, 0, false)
 #define KSTRIP(E, R1, R2, R3, MB) KENTRY(E, R1, R2, R3, MB, 1, false)
 #define KBOTH(E, R1, R2, R3, MB) KROW(E, R1, R2, R3, MB), KSTRIP(E, R1, R2, R3, MB)
@@ -98,9 +101,10 @@ const KernelEntry kKernels[] = {
     // one-CTA-per-SM passes with two warpgroups (plan.cpp PassPlan::nwg)
     KENTRYW(16384, 16, 32, 32, 1, 0, false, 2), KENTRYW(16384, 64, 64, 0, 1, 1, false, 2),
     KENTRYW(16384, 64, 32, 0, 1, 1, false, 2),
-    // two-pass four-step 2^22 with 32-byte runs (experiment: TCFFT_THREE_PASS=0,
-    // TCFFT_SCHUNK_2048 / TCFFT_RCHUNK_2048 = 16384)
-    KENTRYW(16384, 64, 32, 0, 1, 1, true, 2), KENTRYW(16384, 64, 32, 0, 1, 2, false, 2),
+    // single-buffer 16384-element chunks (two CTAs per SM): 1D 16384 rows, 2D
+    // 2048 / 4096 column strips, two-pass 2^22 (strip + twiddle, transposed rows)
+    KONE(16384, 16, 32, 32, 0, false), KONE(16384, 64, 32, 0, 1, false), KONE(16384, 64, 64, 0, 1, false),
+    KONE(16384, 64, 32, 0, 1, true), KONE(16384, 64, 32, 0, 2, false),
     // column strips of 256 columns for N <= 8 (2D nx <= 8 with ny > 256)
     KSTRIP(512, 2, 0, 0, 4),      KSTRIP(1024, 4, 0, 0, 4),     KSTRIP(2048, 8, 0, 0, 4),
     // rows of 4 .. 16 whose element count is not a multiple of 32 (unswizzled staging)
@@ -123,7 +127,7 @@ const KernelEntry* find_kernel(const PassPlan& p) {
   for (int nwg : {p.nwg, 1})
     for (const auto& k : kKernels)
       if (k.E == p.E && k.R1 == r[0] && k.R2 == r[1] && k.R3 == r[2] && k.mode == mode && k.tw4 == tw4 &&
-          k.nwg == nwg)
+          k.nwg == nwg && k.onebuf == p.onebuf)
         return &k;
   return nullptr;
 }
@@ -819,7 +823,7 @@ tcfftResult tcfftDescribePlan(int dims, int nx, int ny, int batch, char* json, s
            ", \"smem_bytes\": " + std::to_string(p.smem_bytes) + ", \"smem_a\": " + std::to_string(p.smem_a) +
            ", \"a_bytes\": " + std::to_string(p.a_bytes) + ", \"tmem_cols\": " + std::to_string(p.tmem_cols) +
            ", \"tmem_a_col\": " + std::to_string(p.tmem_a_cols) +
-           ", \"ctas_per_sm\": " + std::to_string(p.ctas_per_sm) + ", \"nwg\": " + std::to_string(p.nwg) + ", \"planar0\": " + std::to_string(p.planar0) + ", \"a_bufs\": " + std::to_string(p.a_bufs) + ", \"tiles_max\": " +
+           ", \"ctas_per_sm\": " + std::to_string(p.ctas_per_sm) + ", \"nwg\": " + std::to_string(p.nwg) + ", \"planar0\": " + std::to_string(p.planar0) + ", \"a_bufs\": " + std::to_string(p.a_bufs) + ", \"onebuf\": " + std::to_string(p.onebuf) + ", \"tiles_max\": " +
            std::to_string(p.tiles_max) + ", \"stages\": [";
       for (int sidx = 0; sidx < p.S; ++sidx) {
         const auto& t = p.st[sidx];
