@@ -69,7 +69,8 @@ using namespace sm100;
 // kModeStrip4: column strips in, 4D tensor-map store out (three-step pass C)
 // kModeRowU: rows of 4 .. 16 whose batch is not a multiple of 32 elements
 // (unswizzled [total/4][4] staging)
-enum : int { kModeRow = 0, kModeStrip = 1, kModeRowT = 2, kModeStrip4 = 3, kModeRowU = 5 };
+// kModeRowTB: rows of a blocked array in (runtime gather addressing), transposed out
+enum : int { kModeRow = 0, kModeStrip = 1, kModeRowT = 2, kModeStrip4 = 3, kModeRowU = 5, kModeRowTB = 6 };
 
 template <int E_, int R1_, int R2_, int R3_, int MODE_>
 struct Cfg {
@@ -361,6 +362,13 @@ DEVI void issue_load(const CUtensorMap* tm, const KIo& io, int T, int64_t chunk,
         "[%5];" ::"r"(smem_u32(dst)),
         "l"(tm), "r"(0), "r"(0), "r"((int32_t)(chunk * io.n_sub)), "r"(smem_u32(bar))
         : "memory");
+  } else if (io.mode == kIoBlk) {  // C rows of every Bw-wide block of one image, one 4D box
+    const int32_t img = (int32_t)(chunk / io.spi), rb = (int32_t)(chunk % io.spi);
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, "
+        "%5}], [%6];" ::"r"(smem_u32(dst)),
+        "l"(tm), "r"(0), "r"(rb * io.C), "r"(0), "r"(img), "r"(smem_u32(bar))
+        : "memory");
   } else if (io.mode == kIoBoxR) {  // whole > 256-row strip in one 4D box
     const int32_t img = (int32_t)(chunk / io.spi), cb = (int32_t)(chunk % io.spi);
     asm volatile(
@@ -482,7 +490,7 @@ __global__ void __launch_bounds__(128 * NWG, MINB)
   // Transposed-row passes write 16-byte runs whose merging in L2 is sensitive
   // to store timing: they keep the simple (lock-step) chunk loop, measured 1.6x
   // faster for them than the pipelined loop below (round 1).
-  constexpr bool PIPE_OK = MODE != kModeRowT && S >= 2 && NWG == 1 && !ONEBUF;
+  constexpr bool PIPE_OK = MODE != kModeRowT && MODE != kModeRowTB && S >= 2 && NWG == 1 && !ONEBUF;
   constexpr int NT = 128 * NWG;
   static_assert(C::T(0) % NWG == 0 && C::T(S - 1) % NWG == 0 && C::T(S > 1 ? 1 : 0) % NWG == 0, "NWG tiles");
   const bool PIPE = PIPE_OK && p.pipe;

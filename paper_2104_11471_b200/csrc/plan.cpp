@@ -224,8 +224,25 @@ static void box_io(IoDesc& io, int64_t images, int rows, int cols, int C) {
   }
 }
 
+// Flat view of a contiguous chunk stored with the layout of a column-strip
+// staging tile ([rows][W] words, W = the strip width, same swizzle as the
+// strip's box): chunk c occupies elements [c E, (c + 1) E) (two-pass plans
+// write the first pass's output this way: one contiguous store per chunk).
+static void flat_io_w(IoDesc& io, int64_t total, int E, int W) {
+  io.W = W;
+  io.mode = kIoFlat;
+  const int run = W * 4;
+  io.swz = run == 128 ? 0x70 : run == 64 ? 0x30 : run == 32 ? 0x10 : 0;
+  io.box_rows = std::min(E / W, 256);
+  io.n_sub = (E / W) / io.box_rows;
+  io.sub_bytes = io.box_rows * W * 4;
+  io.chunk_rows = E / W;
+  io.total = total;
+  if (io.n_sub > 1 && (total / W) % 256 == 0) io.mode = kIoFlat3;
+}
+
 bool build_pass(PassPlan& p, int kind, int N, int64_t count, int64_t images, int cols, std::string* err,
-                int64_t tw4_total, int tw4_shift) {
+                int64_t tw4_total, int tw4_shift, int blk, int want_E) {
   std::vector<int> rad = choose_radices(N, kind, tw4_total != 0);
   if (rad.empty()) {
     if (err) *err = "no single-pass radix schedule for N=" + std::to_string(N);
@@ -238,6 +255,7 @@ bool build_pass(PassPlan& p, int kind, int N, int64_t count, int64_t images, int
   p.tw4_total = tw4_total;
   p.tw4_shift = tw4_shift;
   const bool row_in = kind == kPassRow || kind == kPassRowT;
+  const bool blk_in = kind == kPassRowTB;  // rows of a blocked array (runtime gather addressing)
   if (kind == kPassRow) {
     p.E = chunk_elems_for(N);
     // Small batches (fewer 4096-element chunks than 4 CTA slots on every SM)
@@ -251,10 +269,10 @@ bool build_pass(PassPlan& p, int kind, int N, int64_t count, int64_t images, int
     p.T = p.E / N;
     p.count = count;
     p.chunks = (count + p.T - 1) / p.T;
-  } else if (kind == kPassRowT) {
+  } else if (kind == kPassRowT || kind == kPassRowTB) {
     // rows of an images x (count/images) x N array, output transposed into
     // images x N x (count/images): >= 4 rows per chunk (>= 16 B output runs)
-    p.E = std::max(chunk_elems_for(N), 4 * N);
+    p.E = want_E ? want_E : std::max(chunk_elems_for(N), 4 * N);
     {
       char key[32];  // experiment hook: TCFFT_RCHUNK_<n>=<elems> overrides the transposed-row chunk size
       std::snprintf(key, sizeof(key), "TCFFT_RCHUNK_%d", N);
@@ -274,13 +292,13 @@ bool build_pass(PassPlan& p, int kind, int N, int64_t count, int64_t images, int
     // chunk, E = N * C * IMG = max(chunk_elems_for(N), 4 N) (C >= 4: >= 16 B runs).
     // (>= 4 columns: TMA boxes move >= 16 bytes per row, so 2D columns of
     // 8192+ rows would need 128 KB chunks: not supported)
-    p.E = std::max(chunk_elems_for(N), 4 * N);
+    p.E = want_E ? want_E : std::max(chunk_elems_for(N), 4 * N);
     // Plain column strips (2D) of 512 .. 2048 use wider chunks: C = 16 / 8 / 8
     // columns (64 / 32 / 32-byte runs) instead of 8 / 4 / 4.  Measured with
     // the lock-step loop: 2D 512^2 0.80 -> 0.88, 1024^2 0.57 -> 0.83 of the
     // HBM roofline (round 1).  Twiddled (four-step) strips keep 4096.
-    if (kind == kPassStrip && !tw4_total && (N == 512 || N == 1024)) p.E = 8192;
-    if (kind == kPassStrip && !tw4_total && N == 2048) p.E = 16384;
+    if (kind == kPassStrip && !tw4_total && !want_E && (N == 512 || N == 1024)) p.E = 8192;
+    if (kind == kPassStrip && !tw4_total && !want_E && N == 2048) p.E = 16384;
     {
       char key[32];  // experiment hook: TCFFT_SCHUNK_<n>=<elems> overrides the strip chunk size
       std::snprintf(key, sizeof(key), "TCFFT_SCHUNK_%d", N);
@@ -323,20 +341,46 @@ bool build_pass(PassPlan& p, int kind, int N, int64_t count, int64_t images, int
   // (pitch_pad_words_out)
   p.pitch = p.pitch_mode ? N + pitch_pad_words(N) : (kind == kPassStripT ? N + pitch_pad_words_out(N) : N);  // words
   const int PW = p.pitch;
+  if (blk_in && (blk <= 0 || N % blk || (N / rad[0]) % blk)) {
+    if (err) *err = "blocked rows: block width must divide N / R1";
+    return false;
+  }
   auto w_in = [&](int tr, int n) -> int32_t {
+    // blocked rows: element n of row tr at (n / Bw) (Bw T) + tr Bw + n % Bw
+    if (blk_in) return (n / blk) * (blk * T) + tr * blk + n % blk;
     return row_in ? tr * PW + n : (tr / C) * NN * C + n * C + tr % C;
   };
   auto w_out = [&](int tr, int n) -> int32_t {
     if (kind == kPassRow) return tr * PW + n;
     if (kind == kPassStripT) return tr * PW + n;
-    if (kind == kPassRowT) return n * T + tr;
+    if (kind == kPassRowT || kind == kPassRowTB) return n * T + tr;
     return (tr / C) * NN * C + n * C + tr % C;
   };
-  p.gstride = (N / rad[0]) * (row_in ? 1 : C);
-  p.ostride = (N / rad[S - 1]) * (kind == kPassRow || kind == kPassStripT ? 1 : (kind == kPassRowT ? T : C));
+  p.gstride = (N / rad[0]) * (blk_in ? T : (row_in ? 1 : C));
+  p.ostride = (N / rad[S - 1]) *
+              (kind == kPassRow || kind == kPassStripT ? 1 : (kind == kPassRowT || kind == kPassRowTB ? T : C));
 
   // ---- TMA / bulk-copy descriptors
-  if (row_in) {
+  if (blk_in) {
+    // images x blocks x rows x Bw: one 4D box {Bw, T rows, all blocks, 1} per
+    // chunk (Bw * T * 4-byte runs)
+    const int rows = (int)(count / images);
+    p.in.mode = kIoBlk;
+    p.in.W = blk;
+    p.in.rows = rows;
+    p.in.cols = N / blk;
+    p.in.images = images;
+    p.in.C = T;
+    p.in.spi = rows / T;
+    p.in.n_sub = 1;
+    p.in.sub_bytes = E * 4;
+    p.in.swz = 0;
+    p.in.total = count * (int64_t)N;
+    if (N / blk > 256 || T > 256 || rows % T) {
+      if (err) *err = "blocked rows: unsupported geometry";
+      return false;
+    }
+  } else if (row_in) {
     const int64_t total = count * (int64_t)N;
     if (p.pitch_mode) {
       p.in.mode = kIoPitch;
@@ -354,7 +398,7 @@ bool build_pass(PassPlan& p, int kind, int N, int64_t count, int64_t images, int
   } else {
     box_io(p.in, images, N, cols, C);
   }
-  if (kind == kPassRowT) {
+  if (kind == kPassRowT || kind == kPassRowTB) {
     box_io(p.out, images, N, p.cols, T);
   } else if (kind == kPassStripT && PW == N) {
     flat_io(p.out, images * (int64_t)N * cols, E, true);  // unpadded: one TMA store per chunk
@@ -649,7 +693,10 @@ bool build_pass(PassPlan& p, int kind, int N, int64_t count, int64_t images, int
     for (int s2 = 0; s2 < S; ++s2) dmax = std::max(dmax, p.st[s2].tiles * p.st[s2].NP);
     const int buf = (std::max(stage_bytes, a_bytes) + 1023) & ~1023;
     const int ob_bytes = buf + bsz + tw4_bytes + 64 + 1024;
-    if (allow && p.ctas_per_sm == 1 && E == 16384 && S >= 2 && p.st[0].tiles % 2 == 0 && dh + a1 <= 256 &&
+    // (row inputs only: strided strip loads need the prefetch of the two-buffer
+    // layout, 2D 2048^2 0.75 -> 0.63 of roofline single-buffered, round 2)
+    if (allow && (kind == kPassRow || kind == kPassRowTB) && p.ctas_per_sm == 1 && E == 16384 && S >= 2 &&
+        p.st[0].tiles % 2 == 0 && dh + a1 <= 256 &&
         dmax <= 256 && 2 * (ob_bytes + 1024) <= 233472) {
       p.onebuf = 1;
       p.nwg = 1;
@@ -717,6 +764,44 @@ static int build_three_step(Plan& plan, int nx, int lg, int64_t batch, std::stri
   return 0;
 }
 
+// Two-pass 1D transform for 2^19 <= N <= 2^22, N = N1 N2 viewed as [N1][N2]
+// (n = N2 n1 + n2, k = k1 + N1 k2):
+//   pass 1: length-N1 FFTs down the columns (strips of C = E1/N1 columns,
+//           C * 4 >= 32-byte runs), twiddle W_N^{n2 k1}; the chunk's staging
+//           tile [k1][C] is stored CONTIGUOUSLY into the workspace, which
+//           therefore holds Y[b][n2 / C][k1][n2 % C] (one flat store per chunk);
+//   pass 2: length-N2 FFTs along k1-rows of that blocked array (one 4D box of
+//           T rows x every block per chunk: C * T * 4-byte runs), transposed
+//           store X[k1 + N1 k2] (T * 4 >= 32-byte runs).
+// Each pass has exactly one strided side; the other side moves long runs, so
+// the TMA engine's per-request cost is paid once per element instead of twice
+// (three passes at >= 64-byte runs before, round 1).
+static int build_two_pass_blocked(Plan& plan, int nx, int lg, int64_t batch, std::string* err) {
+  const int a = lg / 2, b = lg - a;
+  const int N1 = 1 << a, N2 = 1 << b;
+  const int E1 = std::min(16384, 16 * N1), E2 = std::min(16384, 16 * N2);
+  PassPlan p1, p2;
+  if (!build_pass(p1, kPassStrip, N1, 0, batch, N2, err, nx, 0, 0, E1)) return 6;
+  if (p1.IMG != 1 || p1.C * 4 < 32) {
+    if (err) *err = "unsupported two-pass geometry";
+    return 6;
+  }
+  flat_io_w(p1.out, batch * (int64_t)nx, p1.E, p1.C);
+  if (p1.out.swz != p1.swz_out) {
+    if (err) *err = "two-pass: staging swizzle mismatch";
+    return 6;
+  }
+  if (!build_pass(p2, kPassRowTB, N2, batch * (int64_t)N1, batch, 0, err, 0, 0, p1.C, E2)) return 6;
+  p1.ws_out = 1;
+  p2.ws_in = 1;
+  plan.groups = 1;
+  plan.group_bytes = (size_t)batch * (size_t)nx * 4;
+  plan.ws_bytes = plan.group_bytes;
+  plan.passes.push_back(std::move(p1));
+  plan.passes.push_back(std::move(p2));
+  return 0;
+}
+
 int build_plan(Plan& plan, int dims, int nx, int ny, int64_t batch, std::string* err) {
   plan = Plan();
   plan.dims = dims;
@@ -751,6 +836,8 @@ int build_plan(Plan& plan, int dims, int nx, int ny, int64_t batch, std::string*
     }
     // Three passes for N >= 2^19 (every strided access keeps >= 64-byte
     // runs, see below); two passes up to 2^18, whose strips are >= 32 B wide.
+    const char* eb = experiment_env("TCFFT_BLOCKED");
+    if (lg >= 19 && lg <= 22 && (!eb || std::atoi(eb) != 0)) return build_two_pass_blocked(plan, nx, lg, batch, err);
     const char* e3 = experiment_env("TCFFT_THREE_PASS");
     if (lg >= 19 && (!e3 || std::atoi(e3) != 0)) return build_three_step(plan, nx, lg, batch, err);
     const int N1 = 1 << (lg / 2), N2 = 1 << (lg - lg / 2);

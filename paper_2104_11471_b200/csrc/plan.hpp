@@ -23,6 +23,7 @@ enum PassKind : int32_t {
   kPassStrip = 1,  // column strip: element n of column tr at n*C + tr (2D column / four-step pass 1)
   kPassRowT = 2,   // contiguous rows in, transposed columns out (four-step pass 2)
   kPassStripT = 3, // column strip in, each column written as a contiguous row (three-step pass A)
+  kPassRowTB = 4,  // rows of a blocked [block][row][Bw] array in, transposed columns out (two-pass pass 2)
 };
 
 enum IoMode : int32_t {
@@ -32,6 +33,7 @@ enum IoMode : int32_t {
   kIoPitch = 3,  // per-transform 1D bulk copies into a padded staging pitch
   kIoBoxR = 4,   // 4D tensor map {C, 256, rows/256, 1}: a > 256-row strip in ONE box
   kIoFlat3 = 5,  // 3D tensor map {W, 256, n_sub} over [total/W/256][256][W]: one box per chunk
+  kIoBlk = 6,    // 4D tensor map {W, C, blocks, 1} over [images][blocks][rows][W]: C rows of every block
 };
 
 // How one side (load or store) of a pass moves a chunk between HBM and SMEM.
@@ -141,8 +143,9 @@ int chunk_elems_for(int n);
 int pitch_pad_words(int n);
 
 // Builds a pass.  kind/geometry as in PassPlan; returns false on unsupported size.
+// blk: block width Bw of a kPassRowTB input; want_E: chunk size override (0 = default)
 bool build_pass(PassPlan& p, int kind, int N, int64_t count, int64_t images, int cols, std::string* err,
-                int64_t tw4_total = 0, int tw4_shift = 0);
+                int64_t tw4_total = 0, int tw4_shift = 0, int blk = 0, int want_E = 0);
 // Builds the whole plan (host-only, no CUDA calls).
 int build_plan(Plan& plan, int dims, int nx, int ny, int64_t batch, std::string* err);
 

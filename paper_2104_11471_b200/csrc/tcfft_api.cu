@@ -104,7 +104,11 @@ const KernelEntry kKernels[] = {
     // single-buffer 16384-element chunks (two CTAs per SM): 1D 16384 rows, 2D
     // 2048 / 4096 column strips, two-pass 2^22 (strip + twiddle, transposed rows)
     KONE(16384, 16, 32, 32, 0, false), KONE(16384, 64, 32, 0, 1, false), KONE(16384, 64, 64, 0, 1, false),
-    KONE(16384, 64, 32, 0, 1, true), KONE(16384, 64, 32, 0, 2, false),
+    // two-pass 2^19 .. 2^22 (plan.cpp build_two_pass_blocked): strips + twiddle
+    // with a contiguous store, blocked rows in / transposed out
+    KENTRY(8192, 16, 32, 0, 2, 1, true), KENTRYW(16384, 32, 32, 0, 1, 1, true, 2),
+    KENTRYW(16384, 64, 32, 0, 1, 1, true, 2), KENTRYW(16384, 32, 32, 0, 1, 6, false, 2),
+    KENTRYW(16384, 64, 32, 0, 1, 6, false, 2), KONE(16384, 32, 32, 0, 6, false), KONE(16384, 64, 32, 0, 6, false),
     // column strips of 256 columns for N <= 8 (2D nx <= 8 with ny > 256)
     KSTRIP(512, 2, 0, 0, 4),      KSTRIP(1024, 4, 0, 0, 4),     KSTRIP(2048, 8, 0, 0, 4),
     // rows of 4 .. 16 whose element count is not a multiple of 32 (unswizzled staging)
@@ -118,7 +122,8 @@ const KernelEntry* find_kernel(const PassPlan& p) {
   for (int s = 0; s < p.S; ++s) r[s] = p.st[s].R;
   // kPassRow 0, kPassStrip 1, kPassRowT 2 == kernel modes; strip-in / rows-out
   // passes run the strip kernel (their output addressing is all runtime)
-  const int mode = p.kind == tcfft::kPassStripT                          ? (int)tcfft::kPassStrip
+  const int mode = p.kind == tcfft::kPassRowTB                          ? 6 /* kModeRowTB */
+                   : p.kind == tcfft::kPassStripT                        ? (int)tcfft::kPassStrip
                    : (p.kind == tcfft::kPassStrip && p.out.img_split)  ? 3 /* kModeStrip4 */
                    : (p.kind == tcfft::kPassRow && p.N >= 4 && p.N < 32 && p.in.W != 32) ? 5 /* kModeRowU */
                                                                         : p.kind;
@@ -225,9 +230,23 @@ tcfftResult make_tmap(CUtensorMap* tm, const tcfft::IoDesc& io, const void* base
     cuuint64_t strides[2] = {(cuuint64_t)io.W * 4, (cuuint64_t)io.W * 256 * 4};
     cuuint32_t box[3] = {(cuuint32_t)io.W, 256, (cuuint32_t)io.n_sub};
     cuuint32_t es[3] = {1, 1, 1};
+    // (W < 32: the contiguous store of a strip-layout staging tile, plan.cpp flat_io_w)
+    const CUtensorMapSwizzle sw = io.swz == 0x70   ? CU_TENSOR_MAP_SWIZZLE_128B
+                                  : io.swz == 0x30 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                  : io.swz == 0x10 ? CU_TENSOR_MAP_SWIZZLE_32B
+                                                   : CU_TENSOR_MAP_SWIZZLE_NONE;
     r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, const_cast<void*>(base), dims, strides, box, es,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, io.W == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
-            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  } else if (io.mode == tcfft::kIoBlk) {
+    // [images][blocks][rows][W]: box {W, C rows, every block, 1 image}
+    cuuint64_t dims[4] = {(cuuint64_t)io.W, (cuuint64_t)io.rows, (cuuint64_t)io.cols, (cuuint64_t)io.images};
+    cuuint64_t strides[3] = {(cuuint64_t)io.W * 4, (cuuint64_t)io.W * io.rows * 4,
+                             (cuuint64_t)io.W * io.rows * io.cols * 4};
+    cuuint32_t box[4] = {(cuuint32_t)io.W, (cuuint32_t)io.C, (cuuint32_t)io.cols, 1};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, const_cast<void*>(base), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   } else if (io.mode == tcfft::kIoBoxR) {
     const int k = io.rows / 256;
     cuuint64_t dims[4] = {(cuuint64_t)io.cols, 256, (cuuint64_t)k, (cuuint64_t)io.images};
@@ -383,7 +402,7 @@ tcfftResult create(tcfftHandle* out, int dims, int nx, int ny, int batch) {
     k.tw4_nk = k.tw4_s;
     // gather-ahead shifts when each CTA's stores land; the four-step passes
     // write 16-byte runs whose L2 merging is timing sensitive: keep them lockstep
-    k.gather_ahead = (p.tw4_total || p.kind == tcfft::kPassRowT) ? 0 : 1;
+    k.gather_ahead = (p.tw4_total || p.kind == tcfft::kPassRowT || p.kind == tcfft::kPassRowTB) ? 0 : 1;
     if (const char* e = tcfft::experiment_env("TCFFT_GATHER_AHEAD")) k.gather_ahead = std::atoi(e);
     // pipelined loop: measured faster only for the N = 1024 (32, 32) row pass
     // (0.92 vs 0.88 of roofline); slower for the 512 row pass (0.88 vs 0.97),
@@ -413,7 +432,7 @@ tcfftResult create(tcfftHandle* out, int dims, int nx, int ny, int batch) {
     }
     if (const char* e = tcfft::experiment_env("TCFFT_PDL_MASK"))
       if (!((std::atoi(e) >> h->dev.size()) & 1)) k.pdl = 0;
-    if (const char* e = tcfft::experiment_env("TCFFT_PIPE")) k.pipe = std::atoi(e) && p.S >= 2 && p.kind != tcfft::kPassRowT;
+    if (const char* e = tcfft::experiment_env("TCFFT_PIPE")) k.pipe = std::atoi(e) && p.S >= 2 && p.kind != tcfft::kPassRowT && p.kind != tcfft::kPassRowTB;
     // the opt-in maximum: one kernel instance serves plans with different
     // shared-memory requests, occupancy follows each launch's own request
     cudaFuncSetAttribute(d.k->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)prop.sharedMemPerBlockOptin);
@@ -810,7 +829,7 @@ tcfftResult tcfftDescribePlan(int dims, int nx, int ny, int batch, char* json, s
     for (size_t i = 0; i < plan.passes.size(); ++i) {
       const PassPlan& p = plan.passes[i];
       if (i) s += ", ";
-      s += "{\"kind\": \"" + std::string(p.kind == tcfft::kPassRow ? "row" : (p.kind == tcfft::kPassStrip ? "strip" : (p.kind == tcfft::kPassStripT ? "stripT" : "rowT"))) + "\", \"N\": " +
+      s += "{\"kind\": \"" + std::string(p.kind == tcfft::kPassRow ? "row" : (p.kind == tcfft::kPassStrip ? "strip" : (p.kind == tcfft::kPassStripT ? "stripT" : (p.kind == tcfft::kPassRowTB ? "rowTB" : "rowT")))) + "\", \"N\": " +
            std::to_string(p.N) + ", \"E\": " + std::to_string(p.E) + ", \"T\": " + std::to_string(p.T) +
            ", \"C\": " + std::to_string(p.C) + ", \"IMG\": " + std::to_string(p.IMG) +
            ", \"chunks\": " + std::to_string(p.chunks) + ", \"flat\": " + std::to_string(p.flat) +

@@ -273,3 +273,27 @@ def run_threestep(n: int, pairs: np.ndarray) -> np.ndarray:
                 o = emulate_chunk(pc, np.ascontiguousarray(y[b, k2, :, c0: c0 + C]).reshape(-1))
                 out[b, :, k2, c0: c0 + C] = o.reshape(N3, C)
     return out.reshape(B, n)[..., None].view(np.float16).reshape(B, n, 2)
+
+
+def run_twopass_blocked(n: int, pairs: np.ndarray) -> np.ndarray:
+    """Two-pass 1D transform (2^19 <= N <= 2^22, plan.cpp build_two_pass_blocked)
+    of (B, n, 2) fp16: pass 1 column strips of [N1][N2] + twiddle, each chunk's
+    [k1][C] staging tile stored contiguously (workspace Y[b][n2 / C][k1][n2 % C]);
+    pass 2 rows k1 of the blocked workspace (T rows of every block per chunk),
+    transposed store X[k1 + N1 k2]."""
+    B = pairs.shape[0]
+    p1, p2 = PassTables(1, n, 0, B, 0), PassTables(1, n, 0, B, 1)
+    assert p2.d["kind"] == "rowTB", p2.d["kind"]
+    N1, N2, C, T = p1.d["N"], p2.d["N"], p1.d["C"], p2.d["T"]
+    x = np.ascontiguousarray(pairs).view(np.uint32).reshape(B, N1, N2)
+    y = np.empty((B, N2 // C, N1, C), np.uint32)
+    for b in range(B):
+        for cb in range(N2 // C):
+            o = emulate_chunk(p1, np.ascontiguousarray(x[b, :, cb * C: (cb + 1) * C]).reshape(-1), tw4_base=cb * C)
+            y[b, cb] = o.reshape(N1, C)
+    out = np.empty((B, N2, N1), np.uint32)
+    for b in range(B):
+        for r0 in range(0, N1, T):
+            w = np.ascontiguousarray(y[b, :, r0: r0 + T, :]).reshape(-1)  # staging [block][T][C]
+            out[b, :, r0: r0 + T] = emulate_chunk(p2, w).reshape(N2, T)
+    return out.reshape(B, n)[..., None].view(np.float16).reshape(B, n, 2)
