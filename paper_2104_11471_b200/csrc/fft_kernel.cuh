@@ -362,12 +362,12 @@ DEVI void issue_load(const CUtensorMap* tm, const KIo& io, int T, int64_t chunk,
         "[%5];" ::"r"(smem_u32(dst)),
         "l"(tm), "r"(0), "r"(0), "r"((int32_t)(chunk * io.n_sub)), "r"(smem_u32(bar))
         : "memory");
-  } else if (io.mode == kIoBlk) {  // C rows of every Bw-wide block of one image, one 4D box
+  } else if (io.mode == kIoBlk) {  // C-row group rb of every Bw-wide block of one image, one 4D box
     const int32_t img = (int32_t)(chunk / io.spi), rb = (int32_t)(chunk % io.spi);
     asm volatile(
         "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, "
         "%5}], [%6];" ::"r"(smem_u32(dst)),
-        "l"(tm), "r"(0), "r"(rb * io.C), "r"(0), "r"(img), "r"(smem_u32(bar))
+        "l"(tm), "r"(0), "r"(rb), "r"(0), "r"(img), "r"(smem_u32(bar))
         : "memory");
   } else if (io.mode == kIoBoxR) {  // whole > 256-row strip in one 4D box
     const int32_t img = (int32_t)(chunk / io.spi), cb = (int32_t)(chunk % io.spi);
@@ -401,6 +401,8 @@ DEVI void issue_store(const CUtensorMap* tm, const KIo& io, int T, int64_t chunk
     const int nt = (int)min((int64_t)T, io.count - t0);
     for (int i = 0; i < nt; ++i)
       bulk_s2g(const_cast<uint8_t*>(io.gptr) + (t0 + i) * io.gstride_bytes, src + i * io.pitch_bytes, io.sub_bytes);
+  } else if (io.mode == kIoLinear) {  // the staging tile byte for byte, one bulk copy
+    bulk_s2g(const_cast<uint8_t*>(io.gptr) + chunk * (int64_t)io.sub_bytes, src, io.sub_bytes);
   } else if (io.mode == kIoFlat3) {
     asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(tm),
                  "r"(0), "r"(0), "r"((int32_t)(chunk * io.n_sub)), "r"(smem_u32(src))

@@ -224,21 +224,17 @@ static void box_io(IoDesc& io, int64_t images, int rows, int cols, int C) {
   }
 }
 
-// Flat view of a contiguous chunk stored with the layout of a column-strip
-// staging tile ([rows][W] words, W = the strip width, same swizzle as the
-// strip's box): chunk c occupies elements [c E, (c + 1) E) (two-pass plans
-// write the first pass's output this way: one contiguous store per chunk).
-static void flat_io_w(IoDesc& io, int64_t total, int E, int W) {
-  io.W = W;
-  io.mode = kIoFlat;
-  const int run = W * 4;
-  io.swz = run == 128 ? 0x70 : run == 64 ? 0x30 : run == 32 ? 0x10 : 0;
-  io.box_rows = std::min(E / W, 256);
-  io.n_sub = (E / W) / io.box_rows;
-  io.sub_bytes = io.box_rows * W * 4;
-  io.chunk_rows = E / W;
+// The staging tile of a chunk, byte for byte (its swizzle included), to
+// elements [c E, (c + 1) E): one non-tensor bulk copy per chunk (two-pass
+// plans store the first pass's column-strip tiles this way; a tensor map of
+// the strip's 32-byte rows would cost one TMA request per row).
+static void linear_io(IoDesc& io, int64_t total, int E, int swz) {
+  io.mode = kIoLinear;
+  io.W = 0;
+  io.swz = swz;
+  io.n_sub = 1;
+  io.sub_bytes = E * 4;
   io.total = total;
-  if (io.n_sub > 1 && (total / W) % 256 == 0) io.mode = kIoFlat3;
 }
 
 bool build_pass(PassPlan& p, int kind, int N, int64_t count, int64_t images, int cols, std::string* err,
@@ -362,8 +358,8 @@ bool build_pass(PassPlan& p, int kind, int N, int64_t count, int64_t images, int
 
   // ---- TMA / bulk-copy descriptors
   if (blk_in) {
-    // images x blocks x rows x Bw: one 4D box {Bw, T rows, all blocks, 1} per
-    // chunk (Bw * T * 4-byte runs)
+    // images x blocks x rows x Bw: one 4D box {T Bw, 1, all blocks, 1} per
+    // chunk (T-row groups of every block: Bw * T * 4-byte runs)
     const int rows = (int)(count / images);
     p.in.mode = kIoBlk;
     p.in.W = blk;
@@ -376,7 +372,7 @@ bool build_pass(PassPlan& p, int kind, int N, int64_t count, int64_t images, int
     p.in.sub_bytes = E * 4;
     p.in.swz = 0;
     p.in.total = count * (int64_t)N;
-    if (N / blk > 256 || T > 256 || rows % T) {
+    if (N / blk > 256 || T * blk > 256 || rows % T) {
       if (err) *err = "blocked rows: unsupported geometry";
       return false;
     }
@@ -786,12 +782,15 @@ static int build_two_pass_blocked(Plan& plan, int nx, int lg, int64_t batch, std
     if (err) *err = "unsupported two-pass geometry";
     return 6;
   }
-  flat_io_w(p1.out, batch * (int64_t)nx, p1.E, p1.C);
-  if (p1.out.swz != p1.swz_out) {
-    if (err) *err = "two-pass: staging swizzle mismatch";
+  linear_io(p1.out, batch * (int64_t)nx, p1.E, p1.swz_out);
+  if (!build_pass(p2, kPassRowTB, N2, batch * (int64_t)N1, batch, 0, err, 0, 0, p1.C, E2)) return 6;
+  // pass 2 reads the tiles with their swizzle (T-row groups of a block are
+  // whole swizzle atoms, aligned alike in the workspace and in shared memory)
+  p2.in.swz = p2.swz_in = p1.swz_out;
+  if ((p2.T * p1.C * 4) % (p1.C * 4 * 8) != 0) {
+    if (err) *err = "two-pass: row group is not a whole swizzle atom";
     return 6;
   }
-  if (!build_pass(p2, kPassRowTB, N2, batch * (int64_t)N1, batch, 0, err, 0, 0, p1.C, E2)) return 6;
   p1.ws_out = 1;
   p2.ws_in = 1;
   plan.groups = 1;

@@ -33,7 +33,8 @@ enum IoMode : int32_t {
   kIoPitch = 3,  // per-transform 1D bulk copies into a padded staging pitch
   kIoBoxR = 4,   // 4D tensor map {C, 256, rows/256, 1}: a > 256-row strip in ONE box
   kIoFlat3 = 5,  // 3D tensor map {W, 256, n_sub} over [total/W/256][256][W]: one box per chunk
-  kIoBlk = 6,    // 4D tensor map {W, C, blocks, 1} over [images][blocks][rows][W]: C rows of every block
+  kIoBlk = 6,    // 4D tensor map {C*W, 1, blocks, 1} over [images][blocks][rows/C][C*W]: C rows of every block
+  kIoLinear = 7, // the whole staging tile, byte for byte, to/from chunk * E (one non-tensor bulk copy)
 };
 
 // How one side (load or store) of a pass moves a chunk between HBM and SMEM.

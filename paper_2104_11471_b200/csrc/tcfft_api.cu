@@ -205,7 +205,7 @@ CUtensorMapL2promotion box_promotion() {
 
 tcfftResult make_tmap(CUtensorMap* tm, const tcfft::IoDesc& io, const void* base) {
   std::memset(tm, 0, sizeof(*tm));
-  if (io.mode == tcfft::kIoPitch) return TCFFT_SUCCESS;  // raw bulk copies, no tensor map
+  if (io.mode == tcfft::kIoPitch || io.mode == tcfft::kIoLinear) return TCFFT_SUCCESS;  // raw bulk copies
   auto enc = encode_fn();
   if (!enc) return TCFFT_EXEC_FAILED;
   CUresult r;
@@ -238,11 +238,12 @@ tcfftResult make_tmap(CUtensorMap* tm, const tcfft::IoDesc& io, const void* base
     r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, const_cast<void*>(base), dims, strides, box, es,
             CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   } else if (io.mode == tcfft::kIoBlk) {
-    // [images][blocks][rows][W]: box {W, C rows, every block, 1 image}
-    cuuint64_t dims[4] = {(cuuint64_t)io.W, (cuuint64_t)io.rows, (cuuint64_t)io.cols, (cuuint64_t)io.images};
-    cuuint64_t strides[3] = {(cuuint64_t)io.W * 4, (cuuint64_t)io.W * io.rows * 4,
+    // [images][blocks][rows / C][C W]: box {C W, 1 row group, every block, 1 image}
+    const int g = io.C * io.W;
+    cuuint64_t dims[4] = {(cuuint64_t)g, (cuuint64_t)(io.rows / io.C), (cuuint64_t)io.cols, (cuuint64_t)io.images};
+    cuuint64_t strides[3] = {(cuuint64_t)g * 4, (cuuint64_t)io.W * io.rows * 4,
                              (cuuint64_t)io.W * io.rows * io.cols * 4};
-    cuuint32_t box[4] = {(cuuint32_t)io.W, (cuuint32_t)io.C, (cuuint32_t)io.cols, 1};
+    cuuint32_t box[4] = {(cuuint32_t)g, 1, (cuuint32_t)io.cols, 1};
     cuuint32_t es[4] = {1, 1, 1, 1};
     r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, const_cast<void*>(base), dims, strides, box, es,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
