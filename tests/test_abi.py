@@ -46,7 +46,7 @@ def _describe(dims, nx, ny, batch):
 def test_describe_1d_passes(n):
     st, d = _describe(1, n, 0, 8)
     assert st == SUCCESS
-    want = 1 if n <= 16384 else (2 if n <= 1 << 18 else 3)
+    want = 1 if n <= 16384 else (2 if n <= 1 << 22 else 3)  # 2^19..2^22: blocked two-pass
     assert len(d["passes"]) == want
     for p in d["passes"]:
         assert p["E"] % p["N"] == 0 or p["kind"] != "row"
