@@ -240,11 +240,8 @@ static void linear_io(IoDesc& io, int64_t total, int E, int swz) {
 // DFT block matrices of every stage, fp16, UMMA K-major core-matrix order.
 // Full: the real 2R x 2R matrix [[Fr, Fi], [-Fi, Fr]] (K = (m, re/im), N =
 // (j, re/im)); stages with the same radix and planar K share one copy
-// (kernel Cfg::BOFF).  halfb (dual-context kernel, fft_dual.cuh DualB):
-// planar stages of radix >= 32 store only Fr and Fi (R x R each, N = R); the
-// kernel issues the re and im output halves separately and gets -Fi from the
-// instruction descriptor's negate-B bit.
-static void build_bblob(PassPlan& p, bool halfb) {
+// (kernel Cfg::BOFF).
+static void build_bblob(PassPlan& p) {
   const bool planar0 = p.planar0 != 0;
   p.bblob.clear();
   auto planar = [&](int s) { return s >= 1 || planar0; };
@@ -266,8 +263,7 @@ static void build_bblob(PassPlan& p, bool halfb) {
   for (int s = 0; s < p.S; ++s) {
     StageInfo& st = p.st[s];
     const int R = st.R, KP = st.KP, NP = st.NP;
-    const bool hb = halfb && planar(s) && R >= 32;
-    st.b_bytes = hb ? 4 * R * R : KP * NP * 2;
+    st.b_bytes = KP * NP * 2;
 #ifndef TCFFT_NO_BDEDUPE
     if (s >= 1 && planar(s) && planar(s - 1) && p.st[s - 1].R == R) {  // identical planar-K matrix: share it
 #else
@@ -277,11 +273,6 @@ static void build_bblob(PassPlan& p, bool halfb) {
       continue;
     }
     st.b_off = (int)(p.bblob.size() * 2);
-    if (hb) {
-      put(R, R, [&](int m, int j) { return F(R, j, m, false); });
-      put(R, R, [&](int m, int j) { return F(R, j, m, true); });
-      continue;
-    }
     put(KP, NP, [&](int k, int n) {
       if (k >= 2 * R || n >= 2 * R) return 0.0;
       int m, cin;
@@ -618,7 +609,7 @@ bool build_pass(PassPlan& p, int kind, int N, int64_t count, int64_t images, int
   // radix-64 first stages use a planar-K TMEM A operand (kernel Cfg::PLANAR0)
   const bool planar0 = rad[0] == 64;
   p.planar0 = planar0 ? 1 : 0;
-  build_bblob(p, false);
+  build_bblob(p);
   p.tblob.clear();  // twiddles come from the per-row (c, w) recurrence
 
   // ---- shared memory / TMEM budget ---------------------------------------
@@ -696,46 +687,6 @@ bool build_pass(PassPlan& p, int kind, int N, int64_t count, int64_t images, int
     p.nwg = std::max(1, want);
     // registers: 128 per thread at 512 threads per SM
     if (p.nwg > 1) p.ctas_per_sm = std::max(1, std::min(p.ctas_per_sm, 4 / p.nwg));
-  }
-  // Dual-context passes (fft_dual.cuh): when the two-buffer layout leaves one
-  // CTA per SM (16384-element chunks), one CTA of two warpgroups runs two
-  // chunk contexts: staging Z shared, an A / output buffer per context,
-  // halved DFT matrices, 256 TMEM columns per context (stage 1 in two halves).
-  // TCFFT_DUAL=0 (experiment) disables.
-  {
-    const char* e = experiment_env("TCFFT_DUAL");
-    const bool allow = !e || std::atoi(e) != 0;
-    const int dh = p.st[0].tiles / 2 * p.st[0].NP;
-    const int a1 = p.st[0].tiles * (p.st[0].KP / 2);
-    int dmax = 0;
-    for (int s2 = 0; s2 < S; ++s2) dmax = std::max(dmax, p.st[s2].tiles * p.st[s2].NP);
-    if (allow && p.ctas_per_sm == 1 && E == 16384 && S >= 2 && p.st[0].tiles % 2 == 0 && dh + a1 <= 256 &&
-        dmax <= 256) {
-      PassPlan q = p;
-      build_bblob(q, true);
-      const int zb = (stage_bytes + 1023) & ~1023;
-      const int xb = (a_bytes + 1023) & ~1023;
-      const int bb = (((int)q.bblob.size() * 2) + 127) & ~127;
-      const int total = zb + 2 * xb + bb + 2 * tw4_bytes + 128 + 1024;
-      if (total + 1024 <= 233472) {
-        p = q;
-        p.dual = 1;
-        p.nwg = 2;  // two warpgroups = two contexts (256 threads)
-        p.a_bufs = 2;
-        p.smem_in = 0;
-        p.smem_a = zb;
-        p.a_bytes = xb;
-        p.smem_b = zb + 2 * xb;
-        p.smem_t = p.smem_b + bb;
-        p.smem_tw4 = p.smem_t;
-        p.smem_bar = p.smem_tw4 + 2 * tw4_bytes;
-        p.smem_bytes = total;
-        p.tmem_cols = 512;
-        p.tmem_a_cols = dh;
-        p.ctas_per_sm = 1;
-        return true;
-      }
-    }
   }
   // Single-buffer passes (kernel ONEBUF): when the two-buffer layout leaves one
   // CTA per SM (chunks of 16384 elements), one buffer per chunk (staging ==

@@ -113,7 +113,6 @@ struct PassPlan {
   int32_t nwg = 1;           // warpgroups per CTA (2 for one-CTA-per-SM passes with even tile counts)
   int32_t a_bufs;            // 1 or 2 A / output-staging buffers
   int32_t onebuf = 0;        // single-buffer pass (kernel ONEBUF): staging == A buffer, 2 CTAs/SM at E = 16384
-  int32_t dual = 0;          // dual-context pass (fft_dual.cuh): two chunk contexts per CTA, halved DFT matrices
   int32_t tmem_cols_needed;
   std::vector<RowInfo> rows_tab;   // [S][tiles_max][128]
   int32_t tiles_max;

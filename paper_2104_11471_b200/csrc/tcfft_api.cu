@@ -14,7 +14,6 @@
 
 #include "../../include/tcfft_b200.h"
 #include "fft_kernel.cuh"
-#include "fft_dual.cuh"
 #include "plan.hpp"
 
 using tcfft::KParams;
@@ -25,7 +24,7 @@ namespace {
 using KernelFn = void (*)(CUtensorMap, CUtensorMap, KParams);
 
 struct KernelEntry {
-  int E, R1, R2, R3, mode, tw4, nwg, onebuf, dual;
+  int E, R1, R2, R3, mode, tw4, nwg, onebuf;
   const void* fn;
   void (*launch)(dim3, int, cudaStream_t, const CUtensorMap&, const CUtensorMap&, const KParams&);
 };
@@ -58,31 +57,10 @@ void launch_tpl(dim3 grid, int smem, cudaStream_t st, const CUtensorMap& a, cons
   cudaLaunchKernelEx(&cfg, tcfft::fft_pass_kernel<E, R1, R2, R3, MINB, MODE, TW4, NWG, OB>, a, b, p);
 }
 
-template <int E, int R1, int R2, int R3, int MODE, bool TW4>
-void launch_dual(dim3 grid, int smem, cudaStream_t st, const CUtensorMap& a, const CUtensorMap& b, const KParams& p) {
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = grid;
-  cfg.blockDim = dim3(256);
-  cfg.dynamicSmemBytes = (size_t)smem;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = p.pdl ? 1 : 0;
-  cudaLaunchKernelEx(&cfg, tcfft::fft_dual_kernel<E, R1, R2, R3, MODE, TW4>, a, b, p);
-}
-
 #define KENTRYX(E, R1, R2, R3, MB, MODE, TW, NWG, OB)                                                   \
   {                                                                                                     \
-    E, R1, R2, R3, MODE, TW, NWG, OB, 0, (const void*)&tcfft::fft_pass_kernel<E, R1, R2, R3, MB, MODE, TW, NWG, OB>, \
+    E, R1, R2, R3, MODE, TW, NWG, OB, (const void*)&tcfft::fft_pass_kernel<E, R1, R2, R3, MB, MODE, TW, NWG, OB>, \
         &launch_tpl<E, R1, R2, R3, MB, MODE, TW, NWG, OB>                                               \
-  }
-// dual-context passes (fft_dual.cuh, plan.cpp PassPlan::dual): 256 threads, one CTA per SM
-#define KDUAL(E, R1, R2, R3, MODE, TW)                                                                  \
-  {                                                                                                     \
-    E, R1, R2, R3, MODE, TW, 2, 0, 1, (const void*)&tcfft::fft_dual_kernel<E, R1, R2, R3, MODE, TW>,    \
-        &launch_dual<E, R1, R2, R3, MODE, TW>                                                           \
   }
 #define KENTRYW(E, R1, R2, R3, MB, MODE, TW, NWG) KENTRYX(E, R1, R2, R3, MB, MODE, TW, NWG, false)
 #define KENTRY(E, R1, R2, R3, MB, MODE, TW) KENTRYW(E, R1, R2, R3, MB, MODE, TW, 1)
@@ -131,10 +109,6 @@ const KernelEntry kKernels[] = {
     KENTRY(8192, 16, 32, 0, 2, 1, true), KENTRYW(16384, 32, 32, 0, 1, 1, true, 2),
     KENTRYW(16384, 64, 32, 0, 1, 1, true, 2), KENTRYW(16384, 32, 32, 0, 1, 6, false, 2),
     KENTRYW(16384, 64, 32, 0, 1, 6, false, 2), KONE(16384, 32, 32, 0, 6, false), KONE(16384, 64, 32, 0, 6, false),
-    // dual-context 16384-element passes (fft_dual.cuh)
-    KDUAL(16384, 16, 32, 32, 0, false), KDUAL(16384, 64, 32, 0, 1, false), KDUAL(16384, 64, 64, 0, 1, false),
-    KDUAL(16384, 64, 32, 0, 1, true), KDUAL(16384, 32, 32, 0, 1, true), KDUAL(16384, 64, 32, 0, 6, false),
-    KDUAL(16384, 32, 32, 0, 6, false),
     // column strips of 256 columns for N <= 8 (2D nx <= 8 with ny > 256)
     KSTRIP(512, 2, 0, 0, 4),      KSTRIP(1024, 4, 0, 0, 4),     KSTRIP(2048, 8, 0, 0, 4),
     // rows of 4 .. 16 whose element count is not a multiple of 32 (unswizzled staging)
@@ -158,7 +132,7 @@ const KernelEntry* find_kernel(const PassPlan& p) {
   for (int nwg : {p.nwg, 1})
     for (const auto& k : kKernels)
       if (k.E == p.E && k.R1 == r[0] && k.R2 == r[1] && k.R3 == r[2] && k.mode == mode && k.tw4 == tw4 &&
-          k.nwg == nwg && k.onebuf == p.onebuf && k.dual == p.dual)
+          k.nwg == nwg && k.onebuf == p.onebuf)
         return &k;
   return nullptr;
 }
@@ -869,7 +843,7 @@ tcfftResult tcfftDescribePlan(int dims, int nx, int ny, int batch, char* json, s
            ", \"smem_bytes\": " + std::to_string(p.smem_bytes) + ", \"smem_a\": " + std::to_string(p.smem_a) +
            ", \"a_bytes\": " + std::to_string(p.a_bytes) + ", \"tmem_cols\": " + std::to_string(p.tmem_cols) +
            ", \"tmem_a_col\": " + std::to_string(p.tmem_a_cols) +
-           ", \"ctas_per_sm\": " + std::to_string(p.ctas_per_sm) + ", \"nwg\": " + std::to_string(p.nwg) + ", \"planar0\": " + std::to_string(p.planar0) + ", \"a_bufs\": " + std::to_string(p.a_bufs) + ", \"onebuf\": " + std::to_string(p.onebuf) + ", \"dual\": " + std::to_string(p.dual) + ", \"tiles_max\": " +
+           ", \"ctas_per_sm\": " + std::to_string(p.ctas_per_sm) + ", \"nwg\": " + std::to_string(p.nwg) + ", \"planar0\": " + std::to_string(p.planar0) + ", \"a_bufs\": " + std::to_string(p.a_bufs) + ", \"onebuf\": " + std::to_string(p.onebuf) + ", \"tiles_max\": " +
            std::to_string(p.tiles_max) + ", \"stages\": [";
       for (int sidx = 0; sidx < p.S; ++sidx) {
         const auto& t = p.st[sidx];

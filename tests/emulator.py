@@ -34,17 +34,6 @@ class PassTables:
         st = self.d["stages"][s]
         KP, NP = st["KP"], st["NP"]
         R = st["R"]
-        if self.d.get("dual") and (s >= 1 or self.d.get("planar0")) and R >= 32:
-            # dual-context kernel (fft_dual.cuh DualB): only Fr and Fi stored (R x R,
-            # K-major, N = R); the kernel negates Fi through the instruction descriptor
-            k = np.arange(R)[:, None]
-            n = np.arange(R)[None, :]
-            off = (k // 16) * 32 * R + (n % 8) * 16 + (n // 8) * 256 + ((k % 16) // 8) * 128 + (k % 8) * 2
-            fr = self.b[(st["b_off"] + off) // 2].astype(np.float64)
-            fi = self.b[(st["b_off"] + 2 * R * R + off) // 2].astype(np.float64)
-            B = np.zeros((KP, NP))
-            B[:R, :R], B[R:, :R], B[:R, R:], B[R:, R:] = fr, -fi, fi, fr
-            return B
         k = np.arange(KP)[:, None]
         n = np.arange(NP)[None, :]
         off = (k // 16) * 32 * NP + (n % 8) * 16 + (n // 8) * 256 + ((k % 16) // 8) * 128 + (k % 8) * 2
