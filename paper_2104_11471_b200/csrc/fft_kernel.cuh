@@ -53,6 +53,7 @@ struct KParams {
   int32_t tw4_shift;  // exponent uses (column >> tw4_shift) (three-step pass B)
   int32_t tw4_nk;     // number of final-stage k values (N1 / R_S)
   int32_t tw4_s;      // N1 / R_S
+  int32_t late_wait;     // wait for the previous store's shared-memory read after issuing stage 1
   int32_t gather_ahead;  // gather chunk i+1 while chunk i's last MMAs run
   int32_t pipe;          // software-pipelined chunk loop (else the simple lock-step loop)
   int32_t pdl;           // PDL trigger point: 1 = last chunk, 2 = CTA start
@@ -677,13 +678,24 @@ __global__ void __launch_bounds__(128 * NWG, MINB)
           issue_stage_mma<C, 0, 0, T0 / 2, true>(s_a_u, s_b_u, tD, tA);  // first half of stage 1
         } else {
           // the output store that last read this chunk's A buffer is done with it
+          // (late_wait: stage 1 reads TMEM and the B matrices only, so its MMAs
+          // are issued first and the wait overlaps them; the barrier below
+          // holds the writers until thread 0 has passed it)
+          if (!p.late_wait) {
+            if (p.a_stride)
+              bulk_wait_read1();
+            else
+              bulk_wait_read0();
+          }
+          issue_stage_mma<C, 0>(s_a_u, s_b_u, tD, tA);
+        }
+        mma_commit(&bars[1]);
+        if (!ONEBUF && p.late_wait) {
           if (p.a_stride)
             bulk_wait_read1();
           else
             bulk_wait_read0();
-          issue_stage_mma<C, 0>(s_a_u, s_b_u, tD, tA);
         }
-        mma_commit(&bars[1]);
       }
       if constexpr (TW4) {
         // four-step twiddle, strip-base part: A[k] = W_Ntot^{base k}, r = W_Ntot^{base s}
@@ -703,6 +715,7 @@ __global__ void __launch_bounds__(128 * NWG, MINB)
       }
       mbar_wait(&bars[1], mma_phase);
       mma_phase ^= 1;
+      if (!ONEBUF && p.late_wait) __syncthreads();
       tc_fence_after();
 #ifdef TCFFT_TRACE
       if (first && tid == 0 && p.trace) p.trace[blockIdx.x * 8 + 5] = globaltimer_ns();

@@ -590,10 +590,11 @@ bool build_pass(PassPlan& p, int kind, int N, int64_t count, int64_t images, int
       // four-step twiddle W_Ntot^{n2 k1}, n2 = strip base + tr, k1 = k + (N/R_S) j:
       // host part W^{tr k} * (W^{tr s})^j, s = N/R_S; the strip-base part is
       // rebuilt per chunk on the device (kernel tw4 tables).
-      // With tw4_shift (three-step pass B) the exponent is (column >> shift) * k1
-      // and a chunk's C <= 2^shift columns share it: the host part is 1.
+      // With tw4_shift (three-step pass B, 2D split columns) the exponent is
+      // (column >> shift) * k1; chunks start at multiples of C (powers of
+      // two), so (base + tr) >> shift = (base >> shift) + (tr >> shift).
       const int64_t s_ = N / rad[S - 1];
-      const int64_t trx = tw4_shift ? 0 : cur[i].tr;
+      const int64_t trx = cur[i].tr >> tw4_shift;
       double cr, ci, wr, wi;
       root(trx * cur[i].k, tw4_total, &cr, &ci);
       root(trx * s_, tw4_total, &wr, &wi);
@@ -745,7 +746,13 @@ bool build_pass(PassPlan& p, int kind, int N, int64_t count, int64_t images, int
 // (tests/native/strip_io_probe.cu, round 1), so three passes of full-width
 // traffic beat two passes of 16-byte runs (N1 = N2 = 2048) at these sizes.
 static int build_three_step(Plan& plan, int nx, int lg, int64_t batch, std::string* err) {
+  // N3 <= 256 (the 4D natural-order store of pass C); N1, N2 <= 4096 (2^36)
   int a = lg / 3, b = (lg - a) / 2, c = lg - a - b;
+  if (c > 8) {
+    c = 8;
+    a = (lg - c) / 2;
+    b = lg - c - a;
+  }
   if (const char* e = experiment_env("TCFFT_THREE_SPLIT")) {  // experiment hook: "a,b,c" (log2 N1, N2, N3)
     int x, y, z;
     if (std::sscanf(e, "%d,%d,%d", &x, &y, &z) == 3 && x + y + z == lg) a = x, b = y, c = z;
@@ -817,6 +824,52 @@ static int build_two_pass_blocked(Plan& plan, int nx, int lg, int64_t batch, std
   return 0;
 }
 
+// Columns longer than one chunk (2D nx >= 8192), nx = N1 N2 viewed as
+// [N1][N2][ny] (n = N2 n1 + n2, k = k1 + N1 k2), two column passes:
+//   pass 2a: length-N1 FFTs over n1 (column strips of the [N1][N2 ny] image,
+//            column c = n2 ny + y), twiddle W_nx^{n2 k1} = exponent
+//            (c >> log2 ny) k1 -> workspace Y[b][k1][n2][y]
+//   pass 2b: length-N2 FFTs over n2 (strips of each [N2][ny] image (b, k1)),
+//            stored by a 4D tensor map {y, k2 (stride N1 ny), k1 (stride ny),
+//            b (stride nx ny)} straight into X[b][k1 + N1 k2][y]
+// (the three-step plan's passes B and C with a column dimension).
+static int build_2d_split_columns(Plan& plan, int nx, int ny, int64_t batch, std::string* err) {
+  int p = 0, q = 0;
+  while ((1 << p) < nx) ++p;
+  while ((1 << q) < ny) ++q;
+  const int b2 = std::min(8, p - 5), b1 = p - b2;  // N2 = 256 (>= 16-column strips in pass 2b), N1 >= 32
+  if (b1 > 12) {
+    if (err) *err = "2D nx above 2^20 is not supported";
+    return 6;
+  }
+  const int N1 = 1 << b1, N2 = 1 << b2;
+  PassPlan pa, pb;
+  if (!build_pass(pa, kPassStrip, N1, 0, batch, N2 * ny, err, nx, q)) return 6;
+  if (!build_pass(pb, kPassStrip, N2, 0, batch * (int64_t)N1, ny, err)) return 6;
+  if (pa.IMG != 1 || pb.IMG != 1) {
+    if (err) *err = "2D nx >= 8192 needs ny >= " + std::to_string(pb.E / N2) + " (one column strip per chunk)";
+    return 6;
+  }
+  if (pb.in.mode != kIoBox && pb.in.mode != kIoBoxR) {
+    // one strip spans the whole row (C == ny): the flat view build_pass chose
+    // cannot carry the 4D store, use the column box
+    box_io(pb.in, batch * (int64_t)N1, N2, ny, pb.C);
+    pb.out = pb.in;
+    pb.swz_in = pb.swz_out = pb.in.swz;
+    pb.flat = 0;
+  }
+  pb.out.row_stride = (int64_t)N1 * ny;
+  pb.out.img_split = N1;
+  pb.out.img_stride = ny;
+  pb.out.img_stride2 = (int64_t)nx * ny;
+  pa.ws_out = 1;
+  pb.ws_in = 1;
+  plan.ws_bytes = std::max<size_t>(plan.ws_bytes, (size_t)batch * (size_t)nx * (size_t)ny * 4);
+  plan.passes.push_back(std::move(pa));
+  plan.passes.push_back(std::move(pb));
+  return 0;
+}
+
 int build_plan(Plan& plan, int dims, int nx, int ny, int64_t batch, std::string* err) {
   plan = Plan();
   plan.dims = dims;
@@ -845,8 +898,8 @@ int build_plan(Plan& plan, int dims, int nx, int ny, int64_t batch, std::string*
     //   pass 2: length-N2 row FFTs, transposed store X[k1 + N1 k2] -> output
     int lg = 0;
     while ((1 << lg) < nx) ++lg;
-    if (lg > 24) {
-      if (err) *err = "1D sizes above 2^24 are not supported";
+    if (lg > kMaxLog2_1D) {
+      if (err) *err = "1D sizes above 2^" + std::to_string(kMaxLog2_1D) + " are not supported";
       return 6;
     }
     // Three passes for N >= 2^19 (every strided access keeps >= 64-byte
@@ -884,12 +937,30 @@ int build_plan(Plan& plan, int dims, int nx, int ny, int64_t batch, std::string*
   }
   // 2D, row-major (nx, ny): contiguous rows (ny) first, then columns (nx)
   // at stride ny (reference executor.py:180-190).
-  PassPlan rowp, colp;
-  if (!build_pass(rowp, kPassRow, ny, batch * (int64_t)nx, 0, 0, err)) return 6;
-  if (!build_pass(colp, kPassStrip, nx, 0, batch, ny, err)) return 6;
-  plan.passes.push_back(std::move(rowp));
-  plan.passes.push_back(std::move(colp));
-  return 0;
+  if (ny > 16384) {
+    // rows longer than one chunk: the 1D multi-pass plan over batch * nx rows
+    // (its last pass writes the output buffer)
+    Plan rows;
+    const int st = build_plan(rows, 1, ny, 0, batch * (int64_t)nx, err);
+    if (st) return st;
+    for (auto& q : rows.passes) plan.passes.push_back(std::move(q));
+    plan.ws_bytes = rows.ws_bytes;
+    if (rows.groups != 1) {
+      if (err) *err = "2D rows: grouped row plans are not supported";
+      return 6;
+    }
+  } else {
+    PassPlan rowp;
+    if (!build_pass(rowp, kPassRow, ny, batch * (int64_t)nx, 0, 0, err)) return 6;
+    plan.passes.push_back(std::move(rowp));
+  }
+  if (nx <= 4096) {
+    PassPlan colp;
+    if (!build_pass(colp, kPassStrip, nx, 0, batch, ny, err)) return 6;
+    plan.passes.push_back(std::move(colp));
+    return 0;
+  }
+  return build_2d_split_columns(plan, nx, ny, batch, err);
 }
 
 }  // namespace tcfft

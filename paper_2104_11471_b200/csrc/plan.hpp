@@ -17,6 +17,7 @@ namespace tcfft {
 
 constexpr int kMaxStages = 3;
 constexpr int kLanes = 128;  // M of every tcgen05.mma tile
+constexpr int kMaxLog2_1D = 30;  // 1D N <= 2^30 (three-step, N1 N2 N3 with N3 <= 256)
 
 enum PassKind : int32_t {
   kPassRow = 0,    // contiguous transforms: element n of transform tr at tr*N + n

@@ -109,6 +109,8 @@ const KernelEntry kKernels[] = {
     KENTRY(8192, 16, 32, 0, 2, 1, true), KENTRYW(16384, 32, 32, 0, 1, 1, true, 2),
     KENTRYW(16384, 64, 32, 0, 1, 1, true, 2), KENTRYW(16384, 32, 32, 0, 1, 6, false, 2),
     KENTRYW(16384, 64, 32, 0, 1, 6, false, 2), KONE(16384, 32, 32, 0, 6, false), KONE(16384, 64, 32, 0, 6, false),
+    // 2D split columns (plan.cpp build_2d_split_columns): pass 2a of 32 rows
+    KENTRY(4096, 32, 0, 0, 4, 1, true),
     // column strips of 256 columns for N <= 8 (2D nx <= 8 with ny > 256)
     KSTRIP(512, 2, 0, 0, 4),      KSTRIP(1024, 4, 0, 0, 4),     KSTRIP(2048, 8, 0, 0, 4),
     // rows of 4 .. 16 whose element count is not a multiple of 32 (unswizzled staging)
@@ -401,6 +403,11 @@ tcfftResult create(tcfftHandle* out, int dims, int nx, int ny, int batch) {
     k.tw4_shift = p.tw4_shift;
     k.tw4_s = p.N / p.st[p.S - 1].R;
     k.tw4_nk = k.tw4_s;
+    // One-CTA-per-SM passes issue stage 1 before waiting for the previous
+    // chunk's store to have read the A buffer (two-pass 2^22 second pass 0.69
+    // -> 0.71 of roofline; -0.3% for the 4-CTA C2 pass, round 2)
+    k.late_wait = p.ctas_per_sm == 1 ? 1 : 0;
+    if (const char* e = tcfft::experiment_env("TCFFT_LATE_WAIT")) k.late_wait = std::atoi(e);
     // gather-ahead shifts when each CTA's stores land; the four-step passes
     // write 16-byte runs whose L2 merging is timing sensitive: keep them lockstep
     k.gather_ahead = (p.tw4_total || p.kind == tcfft::kPassRowT || p.kind == tcfft::kPassRowTB) ? 0 : 1;
@@ -843,7 +850,7 @@ tcfftResult tcfftDescribePlan(int dims, int nx, int ny, int batch, char* json, s
            ", \"smem_bytes\": " + std::to_string(p.smem_bytes) + ", \"smem_a\": " + std::to_string(p.smem_a) +
            ", \"a_bytes\": " + std::to_string(p.a_bytes) + ", \"tmem_cols\": " + std::to_string(p.tmem_cols) +
            ", \"tmem_a_col\": " + std::to_string(p.tmem_a_cols) +
-           ", \"ctas_per_sm\": " + std::to_string(p.ctas_per_sm) + ", \"nwg\": " + std::to_string(p.nwg) + ", \"planar0\": " + std::to_string(p.planar0) + ", \"a_bufs\": " + std::to_string(p.a_bufs) + ", \"onebuf\": " + std::to_string(p.onebuf) + ", \"tiles_max\": " +
+           ", \"ctas_per_sm\": " + std::to_string(p.ctas_per_sm) + ", \"nwg\": " + std::to_string(p.nwg) + ", \"planar0\": " + std::to_string(p.planar0) + ", \"a_bufs\": " + std::to_string(p.a_bufs) + ", \"onebuf\": " + std::to_string(p.onebuf) + ", \"kernel\": " + std::to_string(find_kernel(p) ? 1 : 0) + ", \"tiles_max\": " +
            std::to_string(p.tiles_max) + ", \"stages\": [";
       for (int sidx = 0; sidx < p.S; ++sidx) {
         const auto& t = p.st[sidx];

@@ -298,3 +298,31 @@ def run_twopass_blocked(n: int, pairs: np.ndarray) -> np.ndarray:
             w = np.ascontiguousarray(y[b, :, r0: r0 + T, :]).reshape(-1)  # staging [block][T][C]
             out[b, :, r0: r0 + T] = emulate_chunk(p2, w).reshape(N2, T)
     return out.reshape(B, n)[..., None].view(np.float16).reshape(B, n, 2)
+
+
+def run_2d_split(nx: int, ny: int, pairs: np.ndarray) -> np.ndarray:
+    """2D transform with split columns (nx >= 8192, plan.cpp
+    build_2d_split_columns) of (B, nx*ny, 2) fp16: the row pass, then pass 2a
+    (length-N1 column strips of [N1][N2 ny] + twiddle, exponent (c >> log2 ny) k1)
+    and pass 2b (strips of each [N2][ny] image (b, k1), stored to row k1 + N1 k2)."""
+    B = pairs.shape[0]
+    p0, pa, pb = (PassTables(2, nx, ny, B, i) for i in range(3))
+    assert p0.d["kind"] == "row" and pa.d["kind"] == "strip" and pb.d["kind"] == "strip"
+    rows = run_pass_row(p0, pairs.reshape(B * nx, ny, 2))
+    N1, N2, shift = pa.d["N"], pb.d["N"], pa.d["tw4_shift"]
+    x = np.ascontiguousarray(rows).view(np.uint32).reshape(B, N1, N2 * ny)
+    C = pa.d["C"]
+    y = np.empty_like(x)
+    for b in range(B):
+        for c0 in range(0, N2 * ny, C):
+            o = emulate_chunk(pa, np.ascontiguousarray(x[b, :, c0: c0 + C]).reshape(-1), tw4_base=c0 >> shift)
+            y[b, :, c0: c0 + C] = o.reshape(N1, C)
+    y = y.reshape(B, N1, N2, ny)
+    C = pb.d["C"]
+    out = np.empty((B, N2, N1, ny), np.uint32)  # row k1 + N1 k2 = [k2][k1]
+    for b in range(B):
+        for k1 in range(N1):
+            for c0 in range(0, ny, C):
+                o = emulate_chunk(pb, np.ascontiguousarray(y[b, k1, :, c0: c0 + C]).reshape(-1))
+                out[b, :, k1, c0: c0 + C] = o.reshape(N2, C)
+    return out.reshape(B, nx * ny)[..., None].view(np.float16).reshape(B, nx * ny, 2)

@@ -42,13 +42,15 @@ def _describe(dims, nx, ny, batch):
     return st, (json.loads(buf.value.decode()) if st == SUCCESS else None)
 
 
-@pytest.mark.parametrize("n", [2, 4, 8, 16, 256, 4096, 16384, 1 << 15, 1 << 18, 1 << 19, 1 << 22, 1 << 24])
+@pytest.mark.parametrize("n", [2, 4, 8, 16, 256, 4096, 16384, 1 << 15, 1 << 18, 1 << 19, 1 << 22, 1 << 24, 1 << 25,
+                               1 << 27, 1 << 30])
 def test_describe_1d_passes(n):
-    st, d = _describe(1, n, 0, 8)
+    st, d = _describe(1, n, 0, 8 if n <= 1 << 24 else 1)
     assert st == SUCCESS
     want = 1 if n <= 16384 else (2 if n <= 1 << 22 else 3)  # 2^19..2^22: blocked two-pass
     assert len(d["passes"]) == want
     for p in d["passes"]:
+        assert p["kernel"] == 1, p  # an sm_100a instantiation exists for every pass
         assert p["E"] % p["N"] == 0 or p["kind"] != "row"
         assert 1 <= p["ctas_per_sm"] <= 4 and p["nwg"] in (1, 2)
         assert p["tmem_cols"] in (32, 64, 128, 256, 512)
@@ -60,12 +62,28 @@ def test_describe_2d_passes(nx, ny):
     st, d = _describe(2, nx, ny, 4)
     assert st == SUCCESS and len(d["passes"]) == 2
     assert d["passes"][0]["kind"] == "row" and d["passes"][1]["kind"] == "strip"
+    assert all(p["kernel"] == 1 for p in d["passes"])
+
+
+@pytest.mark.parametrize("nx,ny,kinds", [(8192, 16, ["row", "strip", "strip"]),
+                                         (1 << 20, 16, ["row", "strip", "strip"]),
+                                         (64, 32768, ["strip", "rowT", "strip"]),
+                                         (4, 1 << 20, ["strip", "rowTB", "strip"]),
+                                         (16384, 32768, ["strip", "rowT", "strip", "strip"])])
+def test_describe_2d_large_sizes(nx, ny, kinds):
+    """Sizes beyond one chunk per column / row (the reference accepts every
+    power of two, plan.py:125-138): split column passes and multi-pass rows."""
+    st, d = _describe(2, nx, ny, 1)
+    assert st == SUCCESS
+    assert [p["kind"] for p in d["passes"]] == kinds
+    assert all(p["kernel"] == 1 for p in d["passes"])
+    assert d["ws_bytes"] >= nx * ny * 4
 
 
 @pytest.mark.parametrize("args,code", [((1, 3, 0, 1), INVALID_SIZE), ((1, 0, 0, 1), INVALID_SIZE),
                                        ((1, 1, 0, 1), INVALID_SIZE), ((2, 8, 6, 1), INVALID_SIZE),
-                                       ((1, 256, 0, 0), INVALID_VALUE), ((1, 1 << 25, 0, 1), NOT_SUPPORTED),
-                                       ((2, 8192, 16, 1), NOT_SUPPORTED)])
+                                       ((1, 256, 0, 0), INVALID_VALUE), ((1, 1 << 31, 0, 1), INVALID_SIZE),
+                                       ((2, 8192, 8, 1), NOT_SUPPORTED), ((2, 1 << 21, 16, 1), NOT_SUPPORTED)])
 def test_describe_rejects_like_the_reference(args, code):
     st, _ = _describe(*args)
     assert st == code

@@ -74,6 +74,59 @@ def test_1d_largest_vs_oracle(n):
     _gates(y, x, n)
 
 
+# ---- sizes beyond 2^24 / 2D columns beyond 4096 / rows beyond 16384 (the
+# reference accepts every power of two, plan.py:116-138)
+def _fp64_check(y, x, nx, ny=None, tol=2e-3):
+    g = R.to_complex(y)
+    f = R.fft64(x, nx, ny)
+    assert np.isfinite(g).all()
+    errs = [R.rel_l2(g[i], f[i]) for i in range(len(g))]
+    assert max(errs) <= tol, errs
+    # Parseval (unnormalised forward transform): sum |X|^2 = N sum |x|^2
+    xc = R.to_complex(x).astype(np.complex128)
+    n = nx * (ny or 1)
+    for i in range(len(g)):
+        ratio = np.sum(np.abs(g[i].astype(np.complex128)) ** 2) / (n * np.sum(np.abs(xc[i]) ** 2))
+        assert abs(ratio - 1) < 5e-3, ratio
+    return max(errs)
+
+
+def test_1d_2pow25_vs_oracle():
+    n = 1 << 25
+    x = R.random_pairs([43, n], 1, n)
+    y = _run(x, n)
+    _gates(y, x, n)
+
+
+@pytest.mark.parametrize("n", [1 << 26, 1 << 27])
+def test_1d_beyond_2pow25_vs_fp64(n):
+    x = R.random_pairs([44, n], 1, n)
+    _fp64_check(_run(x, n), x, n)
+
+
+@pytest.mark.parametrize("nx,ny,batch", [(8192, 16, 2), (8192, 64, 1), (16384, 256, 1), (1 << 16, 32, 1),
+                                         (1 << 20, 16, 1)])
+def test_2d_split_columns_parity(nx, ny, batch):
+    # nx >= 8192: two column passes (plan.cpp build_2d_split_columns)
+    x = R.random_pairs([45, nx, ny], batch, nx * ny)
+    y = _run(x, nx, ny)
+    _gates(y, x, nx, ny)
+
+
+@pytest.mark.parametrize("nx,ny,batch", [(64, 32768, 2), (4, 1 << 20, 1), (16, 1 << 22, 1)])
+def test_2d_multipass_rows_parity(nx, ny, batch):
+    # ny > 16384: the 1D multi-pass plan over the rows, then the column pass
+    x = R.random_pairs([46, nx, ny], batch, nx * ny)
+    y = _run(x, nx, ny)
+    _gates(y, x, nx, ny)
+
+
+def test_2d_split_columns_and_multipass_rows_vs_fp64():
+    nx, ny = 8192, 32768  # four passes: two row passes, two column passes
+    x = R.random_pairs([47, nx, ny], 1, nx * ny)
+    _fp64_check(_run(x, nx, ny), x, nx, ny)
+
+
 @pytest.mark.parametrize("n", [256, 4096, 1 << 16])
 def test_1d_out_of_place_matches_in_place(n):
     x = R.random_pairs([32, n], 5, n)

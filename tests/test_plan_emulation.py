@@ -8,8 +8,8 @@ import pytest
 from paper_2104_11471_b200 import _lib
 
 from oracle import restate as R
-from tests.emulator import (PassTables, emulate_chunk, run_fourstep, run_pass_row, run_pass_strip, run_threestep,
-                            run_twopass_blocked)
+from tests.emulator import (PassTables, emulate_chunk, run_2d_split, run_fourstep, run_pass_row, run_pass_strip,
+                            run_threestep, run_twopass_blocked)
 
 SIZES_1D = [2, 4, 8, 16, 32, 64, 128, 256, 512, 1024, 2048, 4096, 8192, 16384]
 
@@ -106,3 +106,13 @@ def test_threestep_emulation_matches_fft(n):
     e64 = _errs(y, x, n)
     ref_err = 8.5e-4  # the reference's own rel-L2 vs FP64 at 2^22
     assert e64 < ref_err, e64
+
+
+@pytest.mark.parametrize("nx,ny", [(8192, 16), (16384, 16)])
+def test_2d_split_columns_emulation_matches_fft2(nx, ny):
+    """2D nx >= 8192 (two column passes, plan.cpp build_2d_split_columns):
+    the planner's tables replayed on the CPU against the FP64 FFT."""
+    x = R.random_pairs([13, nx, ny], 1, nx * ny)
+    y = run_2d_split(nx, ny, x)
+    e64 = _errs(y, x, nx, ny)
+    assert e64 < 2e-3, e64
