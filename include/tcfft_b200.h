@@ -97,6 +97,25 @@ tcfftResult tcfftDescribePlan(int dims, int nx, int ny, int batch, char* json, s
 tcfftResult tcfftPlanTables(int dims, int nx, int ny, int batch, int pass, void* rows, size_t* rows_bytes,
                             void* bmats, size_t* b_bytes, void* twid, size_t* t_bytes);
 
+/* ---- distributed single transforms (the reference has
+ * no counterpart: SPEC.md:14,467 and PAPER.md:619 leave multi-GPU transforms
+ * out of scope).  One 1D transform of length nx split over `world` ranks
+ * (one process per GPU), four-step N = N1 N2 (N1 = 2^floor(log2(nx)/2)):
+ *   rank g input  : column slab [N1][N2/world], x[N2 n1 + n2], n2 in block g
+ *   pass 0        : tcfftExecDistPass(plan, 0, slab, slab)   column FFTs + twiddle
+ *   exchange      : all-to-all of the slab's N1/world-row blocks (caller, NCCL)
+ *   unpack        : tcfftDistUnpack(plan, world, recv, rows)  -> rows [N1/world][N2]
+ *   pass 1        : tcfftExecDistPass(plan, 1, rows, out)     row FFTs, transposed
+ *   rank g output : [N2][N1/world] = X[k1 + N1 k2], k1 in block g
+ * N1, N2 <= 4096 and divisible by world (N <= 2^24).  Stream-ordered on the
+ * plan's stream like tcfftExecC2C. */
+tcfftResult tcfftPlan1DDist(tcfftHandle* plan, int nx, int rank, int world);
+tcfftResult tcfftExecDistPass(tcfftHandle plan, int pass, const void* idata, void* odata);
+tcfftResult tcfftDistUnpack(tcfftHandle plan, int world, const void* recv, void* rows);
+tcfftResult tcfftDescribeDistPlan(int nx, int rank, int world, char* json, size_t cap);
+tcfftResult tcfftDistPlanTables(int nx, int rank, int world, int pass, void* rows, size_t* rows_bytes, void* bmats,
+                                size_t* b_bytes, void* twid, size_t* t_bytes);
+
 #ifdef __cplusplus
 }
 #endif

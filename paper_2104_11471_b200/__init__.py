@@ -326,9 +326,10 @@ def flops_5nlogn(n_total: int, batch: int) -> float:
 
 from .tcf import read_tcf, write_tcf  # noqa: E402  (TCF1 files, executor.py:203-230)
 from .tensor import BatchedTensor  # noqa: E402  (strided views, executor.py:25-74)
+from .dist import DistPlan  # noqa: E402  (distributed single transforms)
 
 __all__ = [
-    "BatchedTensor", "read_tcf", "write_tcf",
+    "BatchedTensor", "DistPlan", "read_tcf", "write_tcf",
     "ExecuteError", "Plan", "PlanArgumentError", "UnsupportedSizeError", "execute", "execute_host", "flops_5nlogn",
     "plan_1d", "plan_2d", "schedule_radices",
 ]

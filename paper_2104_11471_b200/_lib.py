@@ -29,7 +29,8 @@ EXPORTS = (
     "tcfftPlan1D", "tcfftPlan2D", "tcfftSetStream", "tcfftGetWorkspaceSize", "tcfftExecC2C", "tcfftExecC2CHost",
     "tcfftExecC2CStrided",
     "tcfftDestroy", "tcfftGetErrorString", "tcfftGetVersion", "tcfftDescribePlan", "tcfftPlanTables",
-    "tcfftSetPassMask",
+    "tcfftSetPassMask", "tcfftPlan1DDist", "tcfftExecDistPass", "tcfftDistUnpack", "tcfftDescribeDistPlan",
+    "tcfftDistPlanTables",
 )
 
 
@@ -68,6 +69,12 @@ def load(build_if_missing: bool = True):
     L.tcfftDescribePlan.argtypes = [ci, ci, ci, ci, ctypes.c_char_p, sz]
     L.tcfftPlanTables.argtypes = [ci, ci, ci, ci, ci, vp, ctypes.POINTER(sz), vp, ctypes.POINTER(sz), vp,
                                   ctypes.POINTER(sz)]
+    L.tcfftPlan1DDist.argtypes = [ctypes.POINTER(vp), ci, ci, ci]
+    L.tcfftExecDistPass.argtypes = [vp, ci, vp, vp]
+    L.tcfftDistUnpack.argtypes = [vp, ci, vp, vp]
+    L.tcfftDescribeDistPlan.argtypes = [ci, ci, ci, ctypes.c_char_p, sz]
+    L.tcfftDistPlanTables.argtypes = [ci, ci, ci, ci, vp, ctypes.POINTER(sz), vp, ctypes.POINTER(sz), vp,
+                                      ctypes.POINTER(sz)]
     for name in EXPORTS:
         if name not in ("tcfftGetErrorString",) and hasattr(L, name):
             getattr(L, name).restype = ci
@@ -86,16 +93,32 @@ def describe(dims: int, nx: int, ny: int, batch: int) -> dict:
     return json.loads(buf.value.decode())
 
 
-def plan_tables(dims: int, nx: int, ny: int, batch: int, pass_index: int):
-    """Host tables of one pass as raw bytes: (rows, bmats, twiddles)."""
-    L = load()
+def _tables(call):
     rb, bb, tb = ctypes.c_size_t(0), ctypes.c_size_t(0), ctypes.c_size_t(0)
-    st = L.tcfftPlanTables(dims, nx, ny, batch, pass_index, None, ctypes.byref(rb), None, ctypes.byref(bb), None,
-                           ctypes.byref(tb))
+    st = call(None, ctypes.byref(rb), None, ctypes.byref(bb), None, ctypes.byref(tb))
     if st != TCFFT_SUCCESS:
         raise RuntimeError(error_string(st))
     r = ctypes.create_string_buffer(rb.value)
     b = ctypes.create_string_buffer(bb.value)
     t = ctypes.create_string_buffer(max(tb.value, 1))
-    L.tcfftPlanTables(dims, nx, ny, batch, pass_index, r, ctypes.byref(rb), b, ctypes.byref(bb), t, ctypes.byref(tb))
+    call(r, ctypes.byref(rb), b, ctypes.byref(bb), t, ctypes.byref(tb))
     return r.raw, b.raw, t.raw[: tb.value]
+
+
+def plan_tables(dims: int, nx: int, ny: int, batch: int, pass_index: int):
+    """Host tables of one pass as raw bytes: (rows, bmats, twiddles)."""
+    L = load()
+    return _tables(lambda *a: L.tcfftPlanTables(dims, nx, ny, batch, pass_index, *a))
+
+
+def describe_dist(nx: int, rank: int, world: int) -> dict:
+    """The distributed single-transform plan of one rank (tcfftDescribeDistPlan)."""
+    L = load()
+    buf = ctypes.create_string_buffer(1 << 16)
+    L.tcfftDescribeDistPlan(nx, rank, world, buf, len(buf))
+    return json.loads(buf.value.decode())
+
+
+def dist_plan_tables(nx: int, rank: int, world: int, pass_index: int):
+    L = load()
+    return _tables(lambda *a: L.tcfftDistPlanTables(nx, rank, world, pass_index, *a))

@@ -51,6 +51,7 @@ struct KParams {
   int32_t smem_a, a_stride, smem_b, smem_bar, smem_tw4;
   int64_t tw4_total;  // four-step pass 1: full transform length
   int32_t tw4_shift;  // exponent uses (column >> tw4_shift) (three-step pass B)
+  int64_t tw4_col0;   // global column of the pass's column 0 (distributed plans)
   int32_t tw4_nk;     // number of final-stage k values (N1 / R_S)
   int32_t tw4_s;      // N1 / R_S
   int32_t late_wait;     // wait for the previous store's shared-memory read after issuing stage 1
@@ -703,7 +704,7 @@ __global__ void __launch_bounds__(128 * NWG, MINB)
         // stage-1 MMAs: the last chunk's final epilogue is done with s_tw4, this
         // chunk's reads it after the writer barrier(s).
         if (tid >= 32) {
-          const int64_t base = ((chunk % p.in.spi) * (int64_t)p.in.C) >> p.tw4_shift;
+          const int64_t base = ((chunk % p.in.spi) * (int64_t)p.in.C + p.tw4_col0) >> p.tw4_shift;
           for (int kk = tid - 32; kk <= p.tw4_nk; kk += NT - 32) {
             const int64_t e = (base * (kk < p.tw4_nk ? kk : p.tw4_s)) & (p.tw4_total - 1);
             float sn, cs;
@@ -869,7 +870,7 @@ __global__ void __launch_bounds__(128 * NWG, MINB)
   auto tw4_table = [&](int64_t ch) {
     if constexpr (TW4) {
       // four-step twiddle, strip-base part: A[k] = W_Ntot^{base k}, r = W_Ntot^{base s}
-      const int64_t base = ((ch % p.in.spi) * (int64_t)p.in.C) >> p.tw4_shift;
+      const int64_t base = ((ch % p.in.spi) * (int64_t)p.in.C + p.tw4_col0) >> p.tw4_shift;
       for (int kk = tid; kk <= p.tw4_nk; kk += 128) {
         const int64_t e = (base * (kk < p.tw4_nk ? kk : p.tw4_s)) % p.tw4_total;
         float sn, cs;

@@ -963,4 +963,52 @@ int build_plan(Plan& plan, int dims, int nx, int ny, int64_t batch, std::string*
   return build_2d_split_columns(plan, nx, ny, batch, err);
 }
 
+// Distributed single 1D transform over `world` ranks,
+// N = N1 N2 viewed as [N1][N2] (n = N2 n1 + n2, k = k1 + N1 k2), G = world:
+//   rank g input : the column slab x[N2 n1 + n2], n2 in [g N2/G, (g+1) N2/G),
+//                  stored [N1][N2/G]
+//   pass 0       : length-N1 column FFTs of the slab, twiddle W_N^{n2 k1}
+//                  (global n2 = g N2/G + column: tw4_col0), in place
+//   exchange     : all-to-all of the N1/G-row blocks (NCCL), then the received
+//                  [G][N1/G][N2/G] blocks are unpacked into rows [N1/G][N2]
+//                  (tcfftDistUnpack: G strided device copies)
+//   pass 1       : length-N2 row FFTs, transposed store: rank g output
+//                  [N2][N1/G] = X[k1 + N1 k2] for k1 in [g N1/G, (g+1) N1/G)
+// Both passes are the single-GPU four-step kernels; N1, N2 <= 4096 (N <= 2^24).
+int build_plan_dist(Plan& plan, int nx, int rank, int world, std::string* err) {
+  plan = Plan();
+  plan.dims = 1;
+  plan.nx = nx;
+  plan.batch = 1;
+  auto pow2 = [](int n) { return n >= 1 && (n & (n - 1)) == 0; };
+  if (nx < 2 || !pow2(nx)) {
+    if (err) *err = "sizes must be powers of two >= 2";
+    return 4;
+  }
+  if (!pow2(world) || rank < 0 || rank >= world) {
+    if (err) *err = "world must be a power of two and 0 <= rank < world";
+    return 3;
+  }
+  int lg = 0;
+  while ((1 << lg) < nx) ++lg;
+  const int a = lg / 2, b = lg - a;
+  const int N1 = 1 << a, N2 = 1 << b;
+  if (N1 > 4096 || N2 > 4096 || N1 % world || N2 % world) {
+    if (err) *err = "distributed transforms need N1, N2 <= 4096 divisible by the world size";
+    return 6;
+  }
+  const int cols = N2 / world, rows = N1 / world;
+  PassPlan p0, p1;
+  if (!build_pass(p0, kPassStrip, N1, 0, 1, cols, err, nx, 0)) return 6;
+  if (p0.IMG != 1 || cols % p0.C) {
+    if (err) *err = "distributed transform: column slab narrower than one strip";
+    return 6;
+  }
+  p0.tw4_col0 = (int64_t)rank * cols;
+  if (!build_pass(p1, kPassRowT, N2, rows, 1, 0, err)) return 6;
+  plan.passes.push_back(std::move(p0));
+  plan.passes.push_back(std::move(p1));
+  return 0;
+}
+
 }  // namespace tcfft

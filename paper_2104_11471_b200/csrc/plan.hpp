@@ -101,6 +101,7 @@ struct PassPlan {
   IoDesc in, out;
   int64_t tw4_total;   // four-step pass 1: N of the full transform (extra twiddle), else 0
   int32_t tw4_shift;   // twiddle exponent uses (column >> tw4_shift) (three-step pass B), else 0
+  int64_t tw4_col0 = 0;  // global column of the pass's first column (distributed plans), added to the twiddle base
   int32_t ws_in, ws_out;  // pass reads / writes the plan workspace
   int32_t smem_tw4;
   int64_t total;
@@ -150,5 +151,9 @@ bool build_pass(PassPlan& p, int kind, int N, int64_t count, int64_t images, int
                 int64_t tw4_total = 0, int tw4_shift = 0, int blk = 0, int want_E = 0);
 // Builds the whole plan (host-only, no CUDA calls).
 int build_plan(Plan& plan, int dims, int nx, int ny, int64_t batch, std::string* err);
+// Distributed single transform (rank `rank` of `world`): the two local passes
+// of a four-step N = N1 N2 split by columns (pass 0) and by rows (pass 1); the
+// caller exchanges the data between them (paper_2104_11471_b200/dist.py).
+int build_plan_dist(Plan& plan, int nx, int rank, int world, std::string* err);
 
 }  // namespace tcfft

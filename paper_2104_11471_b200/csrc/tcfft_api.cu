@@ -8,6 +8,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -336,13 +337,21 @@ void release(tcfftPlanImpl* h) {
   delete h;
 }
 
+using PlanBuilder = std::function<int(tcfft::Plan&, std::string*)>;
+
+tcfftResult create_built(tcfftHandle* out, const PlanBuilder& build);
+
 tcfftResult create(tcfftHandle* out, int dims, int nx, int ny, int batch) {
+  return create_built(out, [=](tcfft::Plan& pl, std::string* e) { return tcfft::build_plan(pl, dims, nx, ny, batch, e); });
+}
+
+tcfftResult create_built(tcfftHandle* out, const PlanBuilder& build) {
   if (!out) return TCFFT_INVALID_VALUE;
   *out = nullptr;
   auto* h = new (std::nothrow) tcfftPlanImpl();
   if (!h) return TCFFT_ALLOC_FAILED;
   std::string err;
-  tcfftResult st = map_build_status(tcfft::build_plan(h->plan, dims, nx, ny, batch, &err));
+  tcfftResult st = map_build_status(build(h->plan, &err));
   if (st != TCFFT_SUCCESS) {
     delete h;
     return st;
@@ -401,6 +410,7 @@ tcfftResult create(tcfftHandle* out, int dims, int nx, int ny, int batch) {
     k.smem_tw4 = p.smem_tw4;
     k.tw4_total = p.tw4_total;
     k.tw4_shift = p.tw4_shift;
+    k.tw4_col0 = p.tw4_col0;
     k.tw4_s = p.N / p.st[p.S - 1].R;
     k.tw4_nk = k.tw4_s;
     // One-CTA-per-SM passes issue stage 1 before waiting for the previous
@@ -823,10 +833,11 @@ const char* tcfftGetErrorString(tcfftResult r) {
 
 int tcfftGetVersion(void) { return 100; }
 
-tcfftResult tcfftDescribePlan(int dims, int nx, int ny, int batch, char* json, size_t cap) {
+static tcfftResult describe_json(const PlanBuilder& build, int dims, int nx, int ny, int batch, char* json,
+                                 size_t cap) {
   tcfft::Plan plan;
   std::string err;
-  tcfftResult st = map_build_status(tcfft::build_plan(plan, dims, nx, ny, batch, &err));
+  tcfftResult st = map_build_status(build(plan, &err));
   std::string s;
   if (st != TCFFT_SUCCESS) {
     s = "{\"error\": \"" + err + "\"}";
@@ -844,7 +855,7 @@ tcfftResult tcfftDescribePlan(int dims, int nx, int ny, int batch, char* json, s
            ", \"W\": " + std::to_string(p.in.W) + ", \"pitch\": " + std::to_string(p.pitch) +
            ", \"in_mode\": " + std::to_string(p.in.mode) + ", \"out_mode\": " + std::to_string(p.out.mode) +
            ", \"swz_in\": " + std::to_string(p.swz_in) + ", \"swz_out\": " + std::to_string(p.swz_out) +
-           ", \"tw4_total\": " + std::to_string(p.tw4_total) + ", \"tw4_shift\": " + std::to_string(p.tw4_shift) + ", \"ws_in\": " + std::to_string(p.ws_in) +
+           ", \"tw4_total\": " + std::to_string(p.tw4_total) + ", \"tw4_shift\": " + std::to_string(p.tw4_shift) + ", \"tw4_col0\": " + std::to_string(p.tw4_col0) + ", \"ws_in\": " + std::to_string(p.ws_in) +
            ", \"ws_out\": " + std::to_string(p.ws_out) + ", \"out_cols\": " + std::to_string(p.cols) + ", \"gstride\": " + std::to_string(p.gstride) +
            ", \"ostride\": " + std::to_string(p.ostride) + ", \"swz\": " + std::to_string(p.swz_in) +
            ", \"smem_bytes\": " + std::to_string(p.smem_bytes) + ", \"smem_a\": " + std::to_string(p.smem_a) +
@@ -874,11 +885,11 @@ tcfftResult tcfftDescribePlan(int dims, int nx, int ny, int batch, char* json, s
   return s.size() < cap ? st : TCFFT_INVALID_VALUE;
 }
 
-tcfftResult tcfftPlanTables(int dims, int nx, int ny, int batch, int pass, void* rows, size_t* rows_bytes,
-                            void* bmats, size_t* b_bytes, void* twid, size_t* t_bytes) {
+static tcfftResult plan_tables(const PlanBuilder& build, int pass, void* rows, size_t* rows_bytes, void* bmats,
+                               size_t* b_bytes, void* twid, size_t* t_bytes) {
   tcfft::Plan plan;
   std::string err;
-  tcfftResult st = map_build_status(tcfft::build_plan(plan, dims, nx, ny, batch, &err));
+  tcfftResult st = map_build_status(build(plan, &err));
   if (st != TCFFT_SUCCESS) return st;
   if (pass < 0 || pass >= (int)plan.passes.size()) return TCFFT_INVALID_VALUE;
   const PassPlan& p = plan.passes[pass];
@@ -896,6 +907,69 @@ tcfftResult tcfftPlanTables(int dims, int nx, int ny, int batch, int pass, void*
     *t_bytes = tb;
   }
   return TCFFT_SUCCESS;
+}
+
+tcfftResult tcfftDescribePlan(int dims, int nx, int ny, int batch, char* json, size_t cap) {
+  return describe_json([=](tcfft::Plan& pl, std::string* e) { return tcfft::build_plan(pl, dims, nx, ny, batch, e); },
+                       dims, nx, ny, batch, json, cap);
+}
+
+tcfftResult tcfftPlanTables(int dims, int nx, int ny, int batch, int pass, void* rows, size_t* rows_bytes,
+                            void* bmats, size_t* b_bytes, void* twid, size_t* t_bytes) {
+  return plan_tables([=](tcfft::Plan& pl, std::string* e) { return tcfft::build_plan(pl, dims, nx, ny, batch, e); },
+                     pass, rows, rows_bytes, bmats, b_bytes, twid, t_bytes);
+}
+
+// ---- distributed single transforms (plan.cpp build_plan_dist)
+tcfftResult tcfftPlan1DDist(tcfftHandle* plan, int nx, int rank, int world) {
+  return create_built(plan, [=](tcfft::Plan& pl, std::string* e) { return tcfft::build_plan_dist(pl, nx, rank, world, e); });
+}
+
+tcfftResult tcfftExecDistPass(tcfftHandle plan, int pass, const void* idata, void* odata) {
+  if (!valid(plan)) return TCFFT_INVALID_PLAN;
+  if (pass < 0 || pass >= (int)plan->dev.size() || plan->plan.ws_bytes) return TCFFT_INVALID_VALUE;
+  if (!idata || !odata || !on_plan_device(plan)) return TCFFT_INVALID_VALUE;
+  if ((reinterpret_cast<uintptr_t>(idata) | reinterpret_cast<uintptr_t>(odata)) & 15) return TCFFT_INVALID_VALUE;
+  const PassPlan& p = plan->plan.passes[pass];
+  const DevPass& d = plan->dev[pass];
+  CUtensorMap tin, tout;
+  if (make_tmap(&tin, p.in, idata) != TCFFT_SUCCESS || make_tmap(&tout, p.out, odata) != TCFFT_SUCCESS)
+    return TCFFT_EXEC_FAILED;
+  KParams kp = d.kp;
+  kp.in.gptr = static_cast<const uint8_t*>(idata);
+  kp.out.gptr = static_cast<const uint8_t*>(odata);
+  if (kp.ctr) kp.ctr += 2 * (__atomic_fetch_add(&d.launches, 1u, __ATOMIC_RELAXED) % kTicketSlots);
+  d.k->launch(dim3(d.grid), p.smem_bytes, plan->stream, tin, tout, kp);
+  return cudaGetLastError() == cudaSuccess ? TCFFT_SUCCESS : TCFFT_EXEC_FAILED;
+}
+
+tcfftResult tcfftDistUnpack(tcfftHandle plan, int world, const void* recv, void* rows) {
+  if (!valid(plan)) return TCFFT_INVALID_PLAN;
+  if (plan->plan.passes.size() != 2 || world < 1 || !recv || !rows || !on_plan_device(plan)) return TCFFT_INVALID_VALUE;
+  const PassPlan& p1 = plan->plan.passes[1];
+  // received [G][N1/G][N2/G] (block h from rank h = columns h N2/G ..) -> rows [N1/G][N2]
+  const int64_t N2 = p1.N, nrows = p1.count;
+  if (N2 % world) return TCFFT_INVALID_VALUE;
+  const int64_t bw = N2 / world;
+  for (int h = 0; h < world; ++h) {
+    const char* src = static_cast<const char*>(recv) + (size_t)h * nrows * bw * 4;
+    char* dst = static_cast<char*>(rows) + (size_t)h * bw * 4;
+    if (cudaMemcpy2DAsync(dst, (size_t)N2 * 4, src, (size_t)bw * 4, (size_t)bw * 4, (size_t)nrows,
+                          cudaMemcpyDeviceToDevice, plan->stream) != cudaSuccess)
+      return TCFFT_EXEC_FAILED;
+  }
+  return TCFFT_SUCCESS;
+}
+
+tcfftResult tcfftDescribeDistPlan(int nx, int rank, int world, char* json, size_t cap) {
+  return describe_json([=](tcfft::Plan& pl, std::string* e) { return tcfft::build_plan_dist(pl, nx, rank, world, e); },
+                       1, nx, 0, 1, json, cap);
+}
+
+tcfftResult tcfftDistPlanTables(int nx, int rank, int world, int pass, void* rows, size_t* rows_bytes, void* bmats,
+                                size_t* b_bytes, void* twid, size_t* t_bytes) {
+  return plan_tables([=](tcfft::Plan& pl, std::string* e) { return tcfft::build_plan_dist(pl, nx, rank, world, e); },
+                     pass, rows, rows_bytes, bmats, b_bytes, twid, t_bytes);
 }
 
 }  // extern "C"

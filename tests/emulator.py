@@ -21,10 +21,15 @@ ROW_DT = np.dtype([("gbase", "<i4"), ("addr", "<i4"), ("mp", "<i4"), ("tw", "<i4
 
 
 class PassTables:
-    def __init__(self, dims, nx, ny, batch, index):
-        desc = _lib.describe(dims, nx, ny, batch)
+    def __init__(self, dims, nx, ny, batch, index, dist=None):
+        # dist = (rank, world): a pass of the distributed single-transform plan
+        if dist is None:
+            desc = _lib.describe(dims, nx, ny, batch)
+            rows, b, t = _lib.plan_tables(dims, nx, ny, batch, index)
+        else:
+            desc = _lib.describe_dist(nx, *dist)
+            rows, b, t = _lib.dist_plan_tables(nx, *dist, index)
         self.d = desc["passes"][index]
-        rows, b, t = _lib.plan_tables(dims, nx, ny, batch, index)
         S, tm = len(self.d["stages"]), self.d["tiles_max"]
         self.rows = np.frombuffer(rows, dtype=ROW_DT).reshape(S, tm, 128)
         self.b = np.frombuffer(b, dtype=np.float16)
@@ -326,3 +331,42 @@ def run_2d_split(nx: int, ny: int, pairs: np.ndarray) -> np.ndarray:
                 o = emulate_chunk(pb, np.ascontiguousarray(y[b, k1, :, c0: c0 + C]).reshape(-1))
                 out[b, :, k1, c0: c0 + C] = o.reshape(N2, C)
     return out.reshape(B, nx * ny)[..., None].view(np.float16).reshape(B, nx * ny, 2)
+
+
+class EmulatedDistLocal:
+    """The local steps of paper_2104_11471_b200.dist.DistPlan replayed on the
+    CPU from the planner's own tables (tcfftDistPlanTables): lets CPU ranks
+    (gloo) run the distributed transform end to end."""
+
+    def __init__(self, nx, rank, world):
+        self.p0 = PassTables(1, nx, 0, 1, 0, dist=(rank, world))
+        self.p1 = PassTables(1, nx, 0, 1, 1, dist=(rank, world))
+        self.world = world
+
+    def pass0(self, slab):
+        import torch
+
+        d = self.p0.d
+        n1, C, col0 = d["N"], d["C"], d["tw4_col0"]
+        w = slab.numpy().view(np.uint32).reshape(n1, -1)
+        out = np.empty_like(w)
+        for c0 in range(0, w.shape[1], C):
+            o = emulate_chunk(self.p0, np.ascontiguousarray(w[:, c0: c0 + C]).reshape(-1), tw4_base=col0 + c0)
+            out[:, c0: c0 + C] = o.reshape(n1, C)
+        return torch.from_numpy(out.view(np.float16).reshape(slab.shape))
+
+    def unpack(self, recv, rows):
+        n2 = self.p1.d["N"]
+        G = self.world
+        r = recv.reshape(G, -1, n2 // G, 2)  # [G][N1/G][N2/G]
+        rows.copy_(r.permute(1, 0, 2, 3).reshape(rows.shape))
+        return rows
+
+    def pass1(self, rows, out):
+        import torch
+
+        n2 = self.p1.d["N"]
+        x = rows.numpy().reshape(-1, n2, 2)
+        y = run_pass_rowT(self.p1, x, 1)  # (1, N2, N1/G, 2)
+        out.copy_(torch.from_numpy(np.ascontiguousarray(y)).reshape(out.shape))
+        return out
