@@ -108,7 +108,10 @@ struct Cfg {
   }
   // writer row-block interleave, plan.cpp writer_groups()
   __host__ __device__ static constexpr int HSTEP(int s) {
-    return (R(s) <= 32 ? 128 / R(s) : (E / R(s + 1) >= 4 * R(s) ? 4 : 2)) * SBO(s + 1);
+    return (R(s) == 32 && E / R(s + 1) >= 8 * R(s)
+                ? 8
+                : (R(s) <= 32 ? 128 / R(s) : (E / R(s + 1) >= 8 * R(s) ? 8 : (E / R(s + 1) >= 4 * R(s) ? 4 : 2)))) *
+           SBO(s + 1);
   }
   __host__ __device__ static constexpr int IMOFF(int s) { return 16 * R(s + 1); }
   __host__ __device__ static constexpr int tmax(int a, int b) { return a > b ? a : b; }

@@ -85,8 +85,16 @@ const char* experiment_env(const char* name) {
 }
 
 int writer_groups(int R, int rows_next) {
+  if (R == 32 && rows_next >= 8 * R) return 8;  // (same reason as radix 64 below: 16-column strips)
   if (R <= 32) return kLanes / R;
-  return rows_next >= 4 * R ? 4 : 2;  // a super-block of G groups x R rows must fit the next stage
+  // a super-block of G groups x R rows must fit the next stage.  Eight groups
+  // when they fit: the 8 lanes of a quarter-warp (8 columns of one butterfly
+  // in 8-column strips) then store to 8 consecutive padded row blocks, 8
+  // distinct 16-byte bank groups; with 4 groups rows g and g + 32 share banks
+  // (2-way conflicted writer stores, round 2 ncu: 4.2M excess wavefronts in
+  // the C3 strip pass)
+  if (rows_next >= 8 * R) return 8;
+  return rows_next >= 4 * R ? 4 : 2;
 }
 
 // experiment hook: TCFFT_ROW4096_R64=1 plans 4096-point rows as [64, 64] in
