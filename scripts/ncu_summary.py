@@ -31,8 +31,13 @@ UNIT_SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "usecond": 1,
 
 def report(path: Path):
     raw = path.with_suffix(".raw.csv")
+    rawgz = path.with_suffix(".raw.csv.gz")
     if raw.exists():
         out = raw.read_text()
+    elif rawgz.exists():
+        import gzip
+
+        out = gzip.open(rawgz, "rt").read()
     else:
         out = subprocess.run(["ncu", "-i", str(path), "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
@@ -66,12 +71,13 @@ def main(tag):
     summary = json.loads(summary_path.read_text()) if summary_path.exists() else {}
     lines = [f"# ncu summary ({tag})", "",
              "Captured with `ncu --set full --clock-control none` under gpurun (one B200), "
-             "`scripts/gpu_check.sh`; per-launch values (cold, serialised replays).", "",
+             "`scripts/round_r02.sh` / `scripts/prof_ncu.sh`; per-launch values (cold, serialised replays).", "",
              "| config | kernel | time us | DRAM read MB | DRAM write MB | DRAM % | L1/smem % | smem wavefronts | "
              "ld/st bank conflicts | tensor % | issue % | regs |",
              "|---|---|---|---|---|---|---|---|---|---|---|---|"]
     g = ROOT / "gpurun_out"
-    cfgs = sorted({q.name.split("_")[1] for q in list(g.glob(f"prof_*_{tag}.ncu-rep")) + list(g.glob(f"prof_*_{tag}.raw.csv"))})
+    cfgs = sorted({q.name.split("_")[1] for q in list(g.glob(f"prof_*_{tag}.ncu-rep")) + list(g.glob(f"prof_*_{tag}.raw.csv"))
+                   + list(g.glob(f"prof_*_{tag}.raw.csv.gz"))})
     for cfg in cfgs:
         rep = g / f"prof_{cfg}_{tag}.ncu-rep"
         ks = report(rep)

@@ -6,8 +6,10 @@ compute-sanitizer (memcheck / racecheck / synccheck):
 Covers: 1D single-pass rows 2..16384 (swizzled, unswizzled 4..16-point rows,
 padded-pitch 64..1024, small-batch 2048-element chunks, one-CTA-per-SM
 two-warpgroup 16384), pipelined 1024 rows, ticketed (dynamic) chunk
-scheduling, four-step 2^15..2^18, three-step 2^19..2^22, 2D rows + column
-strips (3D / 4D boxes, 256-column strips for nx <= 8, radix-64 strips),
+scheduling, four-step 2^15..2^18, two-pass blocked 2^19..2^22, three-step
+2^23 / 2^25, 2D rows + column strips (3D / 4D boxes, 256-column strips for
+nx <= 8, radix-64 strips), 2D split columns (nx >= 8192) and multi-pass rows
+(ny > 16384), the distributed plan's two passes + unpack (one rank),
 out-of-place, host-buffer pipeline, strided views."""
 import argparse
 import os
@@ -47,8 +49,20 @@ def main():
               (2048, 2048, 1), (256, 256, 64)]
     if not a.quick:
         cases += [(4096, 4096, 1)]
+    cases += [(1 << 23, None, 1), (8192, 16, 1), (16384, 64, 1), (16, 32768, 1)]
+    if not a.quick:
+        cases += [(1 << 25, None, 1)]
     for c in cases:
         run(*c)
+    # distributed single transform, one rank: pass 0, unpack, pass 1
+    from paper_2104_11471_b200.dist import DistPlan
+
+    for nx in (1 << 14, 1 << 20):
+        dp = DistPlan(nx)
+        out = dp.execute((torch.rand((dp.slab_shape[0], dp.slab_shape[1], 2), device="cuda") * 2 - 1).half())
+        torch.cuda.synchronize()
+        assert torch.isfinite(out.float()).all().item()
+        print("ok dist", nx, flush=True)
     run(4096, None, 64, oop=True)
     # host-buffer pipeline (several slices) and a strided view (scratch path)
     plan = tc.plan_1d(4096, 2048)
