@@ -112,7 +112,24 @@ tcfftResult tcfftPlanTables(int dims, int nx, int ny, int batch, int pass, void*
 tcfftResult tcfftPlan1DDist(tcfftHandle* plan, int nx, int rank, int world);
 tcfftResult tcfftExecDistPass(tcfftHandle plan, int pass, const void* idata, void* odata);
 tcfftResult tcfftDistUnpack(tcfftHandle plan, int world, const void* recv, void* rows);
+/* Fused exchange (world <= 8): pass 0 stores each N1/world-row slice of its
+ * tiles straight into the owning rank's receive buffer (peer memory over
+ * NVLink / CUDA IPC mappings), blocked [N2/C][N1/world][C]; after a
+ * cross-rank barrier pass 1 reads this rank's receive buffer:
+ *   tcfftDistSetPeers(plan, recv, world)       recv[h] = rank h's receive buffer, mapped here
+ *   tcfftExecDistPass(plan, 0, slab, slab)     compute + exchange
+ *   (barrier)  tcfftExecDistPass(plan, 1, recv[rank], out)
+ * tcfftIpc* wrap cudaIpcGetMemHandle / OpenMemHandle / CloseMemHandle
+ * (handle = 64 opaque bytes) for processes that share the buffers. */
+tcfftResult tcfftPlan1DDistFused(tcfftHandle* plan, int nx, int rank, int world);
+tcfftResult tcfftDistSetPeers(tcfftHandle plan, const void* const* recv, int world);
+tcfftResult tcfftIpcGetHandle(const void* dptr, void* handle, size_t cap);
+tcfftResult tcfftIpcOpenHandle(const void* handle, void** dptr);
+tcfftResult tcfftIpcCloseHandle(void* dptr);
 tcfftResult tcfftDescribeDistPlan(int nx, int rank, int world, char* json, size_t cap);
+tcfftResult tcfftDescribeDistPlanFused(int nx, int rank, int world, char* json, size_t cap);
+tcfftResult tcfftDistPlanTablesFused(int nx, int rank, int world, int pass, void* rows, size_t* rows_bytes,
+                                     void* bmats, size_t* b_bytes, void* twid, size_t* t_bytes);
 tcfftResult tcfftDistPlanTables(int nx, int rank, int world, int pass, void* rows, size_t* rows_bytes, void* bmats,
                                 size_t* b_bytes, void* twid, size_t* t_bytes);
 

@@ -30,7 +30,8 @@ EXPORTS = (
     "tcfftExecC2CStrided",
     "tcfftDestroy", "tcfftGetErrorString", "tcfftGetVersion", "tcfftDescribePlan", "tcfftPlanTables",
     "tcfftSetPassMask", "tcfftPlan1DDist", "tcfftExecDistPass", "tcfftDistUnpack", "tcfftDescribeDistPlan",
-    "tcfftDistPlanTables",
+    "tcfftDistPlanTables", "tcfftPlan1DDistFused", "tcfftDistSetPeers", "tcfftIpcGetHandle", "tcfftIpcOpenHandle",
+    "tcfftIpcCloseHandle", "tcfftDescribeDistPlanFused", "tcfftDistPlanTablesFused",
 )
 
 
@@ -75,6 +76,14 @@ def load(build_if_missing: bool = True):
     L.tcfftDescribeDistPlan.argtypes = [ci, ci, ci, ctypes.c_char_p, sz]
     L.tcfftDistPlanTables.argtypes = [ci, ci, ci, ci, vp, ctypes.POINTER(sz), vp, ctypes.POINTER(sz), vp,
                                       ctypes.POINTER(sz)]
+    L.tcfftPlan1DDistFused.argtypes = [ctypes.POINTER(vp), ci, ci, ci]
+    L.tcfftDistSetPeers.argtypes = [vp, ctypes.POINTER(vp), ci]
+    L.tcfftIpcGetHandle.argtypes = [vp, vp, sz]
+    L.tcfftIpcOpenHandle.argtypes = [vp, ctypes.POINTER(vp)]
+    L.tcfftIpcCloseHandle.argtypes = [vp]
+    L.tcfftDescribeDistPlanFused.argtypes = [ci, ci, ci, ctypes.c_char_p, sz]
+    L.tcfftDistPlanTablesFused.argtypes = [ci, ci, ci, ci, vp, ctypes.POINTER(sz), vp, ctypes.POINTER(sz), vp,
+                                           ctypes.POINTER(sz)]
     for name in EXPORTS:
         if name not in ("tcfftGetErrorString",) and hasattr(L, name):
             getattr(L, name).restype = ci
@@ -111,14 +120,15 @@ def plan_tables(dims: int, nx: int, ny: int, batch: int, pass_index: int):
     return _tables(lambda *a: L.tcfftPlanTables(dims, nx, ny, batch, pass_index, *a))
 
 
-def describe_dist(nx: int, rank: int, world: int) -> dict:
-    """The distributed single-transform plan of one rank (tcfftDescribeDistPlan)."""
+def describe_dist(nx: int, rank: int, world: int, fused: bool = False) -> dict:
+    """The distributed single-transform plan of one rank (tcfftDescribeDistPlan[Fused])."""
     L = load()
     buf = ctypes.create_string_buffer(1 << 16)
-    L.tcfftDescribeDistPlan(nx, rank, world, buf, len(buf))
+    (L.tcfftDescribeDistPlanFused if fused else L.tcfftDescribeDistPlan)(nx, rank, world, buf, len(buf))
     return json.loads(buf.value.decode())
 
 
-def dist_plan_tables(nx: int, rank: int, world: int, pass_index: int):
+def dist_plan_tables(nx: int, rank: int, world: int, pass_index: int, fused: bool = False):
     L = load()
-    return _tables(lambda *a: L.tcfftDistPlanTables(nx, rank, world, pass_index, *a))
+    f = L.tcfftDistPlanTablesFused if fused else L.tcfftDistPlanTables
+    return _tables(lambda *a: f(nx, rank, world, pass_index, *a))

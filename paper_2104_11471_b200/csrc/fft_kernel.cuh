@@ -37,6 +37,9 @@ struct KIo {
   int64_t gstride_bytes;  // pitch mode: global distance between transforms (batch_stride * 4)
   int64_t count;        // pitch mode: transforms in the pass
   const uint8_t* gptr;  // pitch mode: raw global pointer, set per execution
+  int32_t npeer;        // peer mode: slices / ranks
+  int64_t peer_blk0;    // peer mode: global column block of chunk 0
+  const uint8_t* peers[8];  // peer mode: every rank's receive buffer (peer / IPC-mapped device pointers)
 };
 
 struct KParams {
@@ -408,6 +411,13 @@ DEVI void issue_store(const CUtensorMap* tm, const KIo& io, int T, int64_t chunk
       bulk_s2g(const_cast<uint8_t*>(io.gptr) + (t0 + i) * io.gstride_bytes, src + i * io.pitch_bytes, io.sub_bytes);
   } else if (io.mode == kIoLinear) {  // the staging tile byte for byte, one bulk copy
     bulk_s2g(const_cast<uint8_t*>(io.gptr) + chunk * (int64_t)io.sub_bytes, src, io.sub_bytes);
+  } else if (io.mode == kIoPeer) {
+    // distributed plans: row slice h of the tile straight into rank h's
+    // receive buffer (over NVLink for a peer GPU), at this chunk's global
+    // column block: the exchange is the pass's own store
+    const int64_t blk = io.peer_blk0 + chunk;
+    for (int h = 0; h < io.npeer; ++h)
+      bulk_s2g(const_cast<uint8_t*>(io.peers[h]) + blk * io.sub_bytes, src + h * io.sub_bytes, io.sub_bytes);
   } else if (io.mode == kIoFlat3) {
     asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(tm),
                  "r"(0), "r"(0), "r"((int32_t)(chunk * io.n_sub)), "r"(smem_u32(src))

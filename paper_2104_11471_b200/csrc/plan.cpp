@@ -983,7 +983,7 @@ int build_plan(Plan& plan, int dims, int nx, int ny, int64_t batch, std::string*
 //   pass 1       : length-N2 row FFTs, transposed store: rank g output
 //                  [N2][N1/G] = X[k1 + N1 k2] for k1 in [g N1/G, (g+1) N1/G)
 // Both passes are the single-GPU four-step kernels; N1, N2 <= 4096 (N <= 2^24).
-int build_plan_dist(Plan& plan, int nx, int rank, int world, std::string* err) {
+int build_plan_dist(Plan& plan, int nx, int rank, int world, std::string* err, bool fused) {
   plan = Plan();
   plan.dims = 1;
   plan.nx = nx;
@@ -1007,13 +1007,42 @@ int build_plan_dist(Plan& plan, int nx, int rank, int world, std::string* err) {
   }
   const int cols = N2 / world, rows = N1 / world;
   PassPlan p0, p1;
-  if (!build_pass(p0, kPassStrip, N1, 0, 1, cols, err, nx, 0)) return 6;
+  // (fused: the wide strips of the single-GPU two-pass plan, >= 32-byte runs)
+  const int E1 = fused ? std::min(16384, 16 * N1) : 0;
+  if (!build_pass(p0, kPassStrip, N1, 0, 1, cols, err, nx, 0, 0, E1)) return 6;
   if (p0.IMG != 1 || cols % p0.C) {
     if (err) *err = "distributed transform: column slab narrower than one strip";
     return 6;
   }
   p0.tw4_col0 = (int64_t)rank * cols;
-  if (!build_pass(p1, kPassRowT, N2, rows, 1, 0, err)) return 6;
+  if (fused) {
+    // Pass 0's staging tile [k1][C] (N1 rows) splits into `world` slices of
+    // N1/world rows; slice h goes byte for byte to rank h's receive buffer at
+    // global column block (rank cols + chunk C) / C, so every rank receives
+    // R[n2 / C][k1 local][n2 % C]: the blocked layout of the single-GPU
+    // two-pass plan, read by the blocked-rows pass (kPassRowTB).
+    const int C = p0.C;
+    const int slice = rows * C * 4;
+    if (rows % 8 || slice % 256 || N2 / C > 256) {
+      if (err) *err = "fused distributed transform: unsupported slice geometry";
+      return 6;
+    }
+    p0.out.mode = kIoPeer;
+    p0.out.n_sub = world;
+    p0.out.sub_bytes = slice;
+    p0.out.npeer = world;
+    p0.out.peer_blk0 = (int64_t)rank * (cols / C);
+    // (p0.out.swz keeps the strip's swizzle: the slices are stored verbatim)
+    const int E2 = std::min(16384, 16 * N2);
+    if (!build_pass(p1, kPassRowTB, N2, rows, 1, 0, err, 0, 0, C, E2)) return 6;
+    p1.in.swz = p1.swz_in = p0.swz_out;
+    if ((p1.T * C * 4) % (C * 4 * 8) != 0) {
+      if (err) *err = "fused distributed transform: row group is not a whole swizzle atom";
+      return 6;
+    }
+  } else {
+    if (!build_pass(p1, kPassRowT, N2, rows, 1, 0, err)) return 6;
+  }
   plan.passes.push_back(std::move(p0));
   plan.passes.push_back(std::move(p1));
   return 0;

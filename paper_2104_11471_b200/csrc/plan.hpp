@@ -36,6 +36,7 @@ enum IoMode : int32_t {
   kIoFlat3 = 5,  // 3D tensor map {W, 256, n_sub} over [total/W/256][256][W]: one box per chunk
   kIoBlk = 6,    // 4D tensor map {C*W, 1, blocks, 1} over [images][blocks][rows/C][C*W]: C rows of every block
   kIoLinear = 7, // the whole staging tile, byte for byte, to/from chunk * E (one non-tensor bulk copy)
+  kIoPeer = 8,   // the staging tile in `npeer` row slices, slice h byte for byte to peer h's buffer (distributed plans)
 };
 
 // How one side (load or store) of a pass moves a chunk between HBM and SMEM.
@@ -52,6 +53,8 @@ struct IoDesc {
   // inner stride img_stride, outer stride img_stride2)
   int64_t row_stride = 0, img_stride = 0, img_stride2 = 0;
   int32_t img_split = 0;
+  int32_t npeer = 0;        // kIoPeer: slices (ranks); slice bytes = sub_bytes
+  int64_t peer_blk0 = 0;    // kIoPeer: global column block of chunk 0
 };
 
 struct StageInfo {
@@ -154,6 +157,10 @@ int build_plan(Plan& plan, int dims, int nx, int ny, int64_t batch, std::string*
 // Distributed single transform (rank `rank` of `world`): the two local passes
 // of a four-step N = N1 N2 split by columns (pass 0) and by rows (pass 1); the
 // caller exchanges the data between them (paper_2104_11471_b200/dist.py).
-int build_plan_dist(Plan& plan, int nx, int rank, int world, std::string* err);
+// fused: pass 0 stores each N1/world-row slice of its staging tile straight
+// into the owning rank's receive buffer (peer memory, kIoPeer) in the blocked
+// layout [N2/C][N1/world][C], pass 1 is the blocked-rows pass (no exchange
+// collective, no unpack).
+int build_plan_dist(Plan& plan, int nx, int rank, int world, std::string* err, bool fused = false);
 
 }  // namespace tcfft

@@ -112,6 +112,10 @@ const KernelEntry kKernels[] = {
     KENTRYW(16384, 64, 32, 0, 1, 6, false, 2), KONE(16384, 32, 32, 0, 6, false), KONE(16384, 64, 32, 0, 6, false),
     // 2D split columns (plan.cpp build_2d_split_columns): pass 2a of 32 rows
     KENTRY(4096, 32, 0, 0, 4, 1, true),
+    // fused distributed plans of 2^14 .. 2^18 (plan.cpp build_plan_dist): wide
+    // twiddled strips and blocked rows of 128 .. 512
+    KENTRY(2048, 8, 16, 0, 4, 1, true), KENTRY(2048, 8, 16, 0, 4, 6, false), KENTRY(4096, 16, 16, 0, 4, 6, false),
+    KENTRY(8192, 16, 32, 0, 2, 6, false),
     // column strips of 256 columns for N <= 8 (2D nx <= 8 with ny > 256)
     KSTRIP(512, 2, 0, 0, 4),      KSTRIP(1024, 4, 0, 0, 4),     KSTRIP(2048, 8, 0, 0, 4),
     // rows of 4 .. 16 whose element count is not a multiple of 32 (unswizzled staging)
@@ -208,7 +212,8 @@ CUtensorMapL2promotion box_promotion() {
 
 tcfftResult make_tmap(CUtensorMap* tm, const tcfft::IoDesc& io, const void* base) {
   std::memset(tm, 0, sizeof(*tm));
-  if (io.mode == tcfft::kIoPitch || io.mode == tcfft::kIoLinear) return TCFFT_SUCCESS;  // raw bulk copies
+  if (io.mode == tcfft::kIoPitch || io.mode == tcfft::kIoLinear || io.mode == tcfft::kIoPeer)
+    return TCFFT_SUCCESS;  // raw bulk copies
   auto enc = encode_fn();
   if (!enc) return TCFFT_EXEC_FAILED;
   CUresult r;
@@ -300,6 +305,8 @@ tcfft::KIo to_kio(const tcfft::IoDesc& io, const PassPlan& p) {
   k.pitch_bytes = p.pitch * 4;
   k.gstride_bytes = (int64_t)io.sub_bytes;  // contiguous transforms; strided exec overrides
   k.count = p.count;
+  k.npeer = io.npeer;
+  k.peer_blk0 = io.peer_blk0;
   return k;
 }
 
@@ -925,6 +932,64 @@ tcfftResult tcfftPlan1DDist(tcfftHandle* plan, int nx, int rank, int world) {
   return create_built(plan, [=](tcfft::Plan& pl, std::string* e) { return tcfft::build_plan_dist(pl, nx, rank, world, e); });
 }
 
+tcfftResult tcfftPlan1DDistFused(tcfftHandle* plan, int nx, int rank, int world) {
+  if (world > 8) return TCFFT_NOT_SUPPORTED;
+  return create_built(plan,
+                      [=](tcfft::Plan& pl, std::string* e) { return tcfft::build_plan_dist(pl, nx, rank, world, e, true); });
+}
+
+tcfftResult tcfftDistSetPeers(tcfftHandle plan, const void* const* recv, int world) {
+  if (!valid(plan)) return TCFFT_INVALID_PLAN;
+  if (plan->dev.empty() || plan->plan.passes[0].out.mode != tcfft::kIoPeer || !recv ||
+      world != plan->plan.passes[0].out.npeer)
+    return TCFFT_INVALID_VALUE;
+  for (int h = 0; h < world; ++h) {
+    if (!recv[h] || (reinterpret_cast<uintptr_t>(recv[h]) & 15)) return TCFFT_INVALID_VALUE;
+    plan->dev[0].kp.out.peers[h] = static_cast<const uint8_t*>(recv[h]);
+  }
+  return TCFFT_SUCCESS;
+}
+
+tcfftResult tcfftIpcGetHandle(const void* dptr, void* handle, size_t cap) {
+  if (!dptr || !handle || cap < sizeof(cudaIpcMemHandle_t)) return TCFFT_INVALID_VALUE;
+  cudaIpcMemHandle_t h;
+  if (cudaIpcGetMemHandle(&h, const_cast<void*>(dptr)) != cudaSuccess) {
+    cudaGetLastError();
+    return TCFFT_EXEC_FAILED;
+  }
+  std::memcpy(handle, &h, sizeof(h));
+  return TCFFT_SUCCESS;
+}
+
+tcfftResult tcfftIpcOpenHandle(const void* handle, void** dptr) {
+  if (!handle || !dptr) return TCFFT_INVALID_VALUE;
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof(h));
+  if (cudaIpcOpenMemHandle(dptr, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+    cudaGetLastError();
+    return TCFFT_EXEC_FAILED;
+  }
+  return TCFFT_SUCCESS;
+}
+
+tcfftResult tcfftIpcCloseHandle(void* dptr) {
+  if (!dptr) return TCFFT_INVALID_VALUE;
+  return cudaIpcCloseMemHandle(dptr) == cudaSuccess ? TCFFT_SUCCESS : TCFFT_EXEC_FAILED;
+}
+
+tcfftResult tcfftDescribeDistPlanFused(int nx, int rank, int world, char* json, size_t cap) {
+  return describe_json(
+      [=](tcfft::Plan& pl, std::string* e) { return tcfft::build_plan_dist(pl, nx, rank, world, e, true); }, 1, nx, 0,
+      1, json, cap);
+}
+
+tcfftResult tcfftDistPlanTablesFused(int nx, int rank, int world, int pass, void* rows, size_t* rows_bytes,
+                                     void* bmats, size_t* b_bytes, void* twid, size_t* t_bytes) {
+  return plan_tables(
+      [=](tcfft::Plan& pl, std::string* e) { return tcfft::build_plan_dist(pl, nx, rank, world, e, true); }, pass, rows,
+      rows_bytes, bmats, b_bytes, twid, t_bytes);
+}
+
 tcfftResult tcfftExecDistPass(tcfftHandle plan, int pass, const void* idata, void* odata) {
   if (!valid(plan)) return TCFFT_INVALID_PLAN;
   if (pass < 0 || pass >= (int)plan->dev.size() || plan->plan.ws_bytes) return TCFFT_INVALID_VALUE;
@@ -932,6 +997,7 @@ tcfftResult tcfftExecDistPass(tcfftHandle plan, int pass, const void* idata, voi
   if ((reinterpret_cast<uintptr_t>(idata) | reinterpret_cast<uintptr_t>(odata)) & 15) return TCFFT_INVALID_VALUE;
   const PassPlan& p = plan->plan.passes[pass];
   const DevPass& d = plan->dev[pass];
+  if (p.out.mode == tcfft::kIoPeer && !d.kp.out.peers[0]) return TCFFT_INVALID_VALUE;  // tcfftDistSetPeers first
   CUtensorMap tin, tout;
   if (make_tmap(&tin, p.in, idata) != TCFFT_SUCCESS || make_tmap(&tout, p.out, odata) != TCFFT_SUCCESS)
     return TCFFT_EXEC_FAILED;

@@ -21,14 +21,14 @@ ROW_DT = np.dtype([("gbase", "<i4"), ("addr", "<i4"), ("mp", "<i4"), ("tw", "<i4
 
 
 class PassTables:
-    def __init__(self, dims, nx, ny, batch, index, dist=None):
+    def __init__(self, dims, nx, ny, batch, index, dist=None, fused=False):
         # dist = (rank, world): a pass of the distributed single-transform plan
         if dist is None:
             desc = _lib.describe(dims, nx, ny, batch)
             rows, b, t = _lib.plan_tables(dims, nx, ny, batch, index)
         else:
-            desc = _lib.describe_dist(nx, *dist)
-            rows, b, t = _lib.dist_plan_tables(nx, *dist, index)
+            desc = _lib.describe_dist(nx, *dist, fused=fused)
+            rows, b, t = _lib.dist_plan_tables(nx, *dist, index, fused=fused)
         self.d = desc["passes"][index]
         S, tm = len(self.d["stages"]), self.d["tiles_max"]
         self.rows = np.frombuffer(rows, dtype=ROW_DT).reshape(S, tm, 128)
@@ -369,4 +369,48 @@ class EmulatedDistLocal:
         x = rows.numpy().reshape(-1, n2, 2)
         y = run_pass_rowT(self.p1, x, 1)  # (1, N2, N1/G, 2)
         out.copy_(torch.from_numpy(np.ascontiguousarray(y)).reshape(out.shape))
+        return out
+
+
+class EmulatedDistLocalFused:
+    """The fused distributed plan's local steps replayed on the CPU
+    (tcfftDistPlanTablesFused): pass 0 returns the N1/G-row slices of every
+    staging tile, arranged [G][blocks][N1/G][C] (what the kernel's peer stores
+    deliver to each rank); pass 1 is the blocked-rows pass over the received
+    [N2/C][N1/G][C] buffer."""
+
+    fused = True
+
+    def __init__(self, nx, rank, world):
+        self.p0 = PassTables(1, nx, 0, 1, 0, dist=(rank, world), fused=True)
+        self.p1 = PassTables(1, nx, 0, 1, 1, dist=(rank, world), fused=True)
+        self.world = world
+        assert self.p1.d["kind"] == "rowTB"
+
+    def pass0(self, slab):
+        import torch
+
+        d = self.p0.d
+        n1, C, col0 = d["N"], d["C"], d["tw4_col0"]
+        G = self.world
+        w = slab.numpy().view(np.uint32).reshape(n1, -1)
+        nb = w.shape[1] // C
+        send = np.empty((G, nb, n1 // G, C), np.uint32)
+        for cb in range(nb):
+            o = emulate_chunk(self.p0, np.ascontiguousarray(w[:, cb * C: (cb + 1) * C]).reshape(-1),
+                              tw4_base=col0 + cb * C).reshape(n1, C)
+            send[:, cb] = o.reshape(G, n1 // G, C)
+        return torch.from_numpy(send.reshape(-1)[..., None].view(np.float16).reshape(-1, 2))
+
+    def pass1(self, recv, out):
+        import torch
+
+        C, T, n2 = self.p0.d["C"], self.p1.d["T"], self.p1.d["N"]
+        y = recv.numpy().view(np.uint32).reshape(n2 // C, -1, C)  # [blocks][N1/G][C]
+        rows = y.shape[1]
+        res = np.empty((n2, rows), np.uint32)
+        for r0 in range(0, rows, T):
+            wv = np.ascontiguousarray(y[:, r0: r0 + T, :]).reshape(-1)
+            res[:, r0: r0 + T] = emulate_chunk(self.p1, wv).reshape(n2, T)
+        out.copy_(torch.from_numpy(res.reshape(-1)[..., None].view(np.float16).reshape(out.shape)))
         return out

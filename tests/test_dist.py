@@ -55,16 +55,18 @@ def test_scatter_gather_roundtrip():
     assert all((X[:, g * (n1 // world):(g + 1) * (n1 // world)] == g).all() for g in range(world))
 
 
-def _worker(rank, world, port, nx, q):
+def _worker(rank, world, port, nx, q, fused=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         from paper_2104_11471_b200.dist import DistPlan
-        from tests.emulator import EmulatedDistLocal
+        from tests.emulator import EmulatedDistLocal, EmulatedDistLocalFused
 
         x = R.random_pairs([71, nx], 1, nx)[0]  # every rank regenerates the global input
-        plan = DistPlan(nx, local=EmulatedDistLocal(nx, rank, world))
+        local = (EmulatedDistLocalFused if fused else EmulatedDistLocal)(nx, rank, world)
+        plan = DistPlan(nx, local=local)
+        assert plan.fused == fused
         slab = torch.from_numpy(scatter_slab(x, rank, world))
         out = plan.execute(slab)
         parts = [torch.empty_like(out) for _ in range(world)]
@@ -76,12 +78,16 @@ def _worker(rank, world, port, nx, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("nx,world", [(1 << 14, 2), (1 << 16, 2)])
-def test_dist_transform_gloo_emulated(nx, world):
+@pytest.mark.parametrize("nx,world,fused", [(1 << 14, 2, False), (1 << 16, 2, False), (1 << 14, 2, True),
+                                            (1 << 16, 2, True), (1 << 16, 4, True)])
+def test_dist_transform_gloo_emulated(nx, world, fused):
+    """fused: the peer-store layout (each rank's pass-0 slices land blocked
+    [N2/C][N1/G][C] in the owning rank, read by the blocked-rows pass), the
+    kernel's stores modelled by an all-to-all of the slices."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, nx, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, nx, q, fused)) for r in range(world)]
     for p in procs:
         p.start()
     X = q.get(timeout=600)
@@ -97,11 +103,12 @@ def test_dist_transform_gloo_emulated(nx, world):
 
 
 # ---------------------------------------------------------------- GPU leg
-def _gpu_run(nx, rank, world):
+def _gpu_run(nx, rank, world, fused=None):
     from paper_2104_11471_b200.dist import DistPlan
 
     x = R.random_pairs([72, nx], 1, nx)[0]
-    plan = DistPlan(nx)
+    plan = DistPlan(nx, fused=fused)
+    assert fused is None or plan.fused == fused
     slab = torch.from_numpy(scatter_slab(x, rank, world)).cuda()
     out = plan.execute(slab)
     torch.cuda.synchronize()
@@ -124,13 +131,13 @@ def test_dist_transform_world1_gpu(nx):
         assert np.array_equal(t.cpu().numpy()[0].view(np.uint16), X.view(np.uint16))
 
 
-def _gpu_worker(rank, world, port, nx, q):
+def _gpu_worker(rank, world, port, nx, q, fused=None):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     torch.cuda.set_device(0)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        x, out = _gpu_run(nx, rank, world)
+        x, out = _gpu_run(nx, rank, world, fused)
         parts = [torch.empty_like(torch.from_numpy(out)) for _ in range(world)]
         dist.all_gather(parts, torch.from_numpy(out))
         if rank == 0:
@@ -140,13 +147,17 @@ def _gpu_worker(rank, world, port, nx, q):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("nx", [1 << 16, 1 << 22])
-def test_dist_transform_two_ranks_one_gpu(nx):
+@pytest.mark.parametrize("nx,fused", [(1 << 16, False), (1 << 22, False), (1 << 16, True), (1 << 20, True),
+                                      (1 << 22, True), (1 << 24, None)])
+def test_dist_transform_two_ranks_one_gpu(nx, fused):
+    """Two ranks sharing one GPU.  fused: pass 0 stores its slices into both
+    ranks' receive buffers through CUDA IPC mappings (the peer-memory path,
+    here on one device); None: the default choice (2^24: NCCL-style exchange)."""
     world = 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_gpu_worker, args=(r, world, port, nx, q)) for r in range(world)]
+    procs = [ctx.Process(target=_gpu_worker, args=(r, world, port, nx, q, fused)) for r in range(world)]
     for p in procs:
         p.start()
     X = q.get(timeout=600)
