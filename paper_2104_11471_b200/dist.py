@@ -212,6 +212,12 @@ class DistPlan:
         if hasattr(self.local, "destroy"):
             self.local.destroy()
 
+    def __del__(self):
+        try:
+            self.destroy()
+        except Exception:
+            pass
+
     def _exchange(self, send):
         """All-to-all of equal row blocks (NCCL for CUDA tensors; CPU tensors
         and gloo groups stage through host memory)."""
