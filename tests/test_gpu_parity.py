@@ -248,7 +248,8 @@ def test_config_c3_n2pow22_batch64():
     _config_check(1 << 22, None, 64, 8)
 
 
-@pytest.mark.parametrize("nx,ny,batch", [(4096, None, 2048), (256, None, 3000), (1 << 16, None, 3), (512, 512, 5)])
+@pytest.mark.parametrize("nx,ny,batch", [(4096, None, 2048), (256, None, 3000), (1 << 16, None, 3), (512, 512, 5),
+                                         (1 << 22, None, 9), (1 << 25, None, 1), (8192, 64, 3), (64, 32768, 2)])
 def test_execute_host_matches_device_path(nx, ny, batch):
     """tcfftExecC2CHost (sliced, pipelined host-buffer path) == device path."""
     tc = _tc()
