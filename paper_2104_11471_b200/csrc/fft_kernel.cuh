@@ -370,13 +370,15 @@ DEVI void issue_load(const CUtensorMap* tm, const KIo& io, int T, int64_t chunk,
         "[%5];" ::"r"(smem_u32(dst)),
         "l"(tm), "r"(0), "r"(0), "r"((int32_t)(chunk * io.n_sub)), "r"(smem_u32(bar))
         : "memory");
-  } else if (io.mode == kIoBlk) {  // C-row group rb of every Bw-wide block of one image, one 4D box
+  } else if (io.mode == kIoBlk) {  // C-row group rb of every Bw-wide block of one image, 4D boxes of <= 256 blocks
     const int32_t img = (int32_t)(chunk / io.spi), rb = (int32_t)(chunk % io.spi);
-    asm volatile(
-        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, "
-        "%5}], [%6];" ::"r"(smem_u32(dst)),
-        "l"(tm), "r"(0), "r"(rb), "r"(0), "r"(img), "r"(smem_u32(bar))
-        : "memory");
+    const int32_t bpb = io.box_rows;  // blocks per box
+    for (int i = 0; i < io.n_sub; ++i)
+      asm volatile(
+          "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, "
+          "%5}], [%6];" ::"r"(smem_u32(dst + i * io.sub_bytes)),
+          "l"(tm), "r"(0), "r"(rb), "r"(i * bpb), "r"(img), "r"(smem_u32(bar))
+          : "memory");
   } else if (io.mode == kIoBoxR) {  // whole > 256-row strip in one 4D box
     const int32_t img = (int32_t)(chunk / io.spi), cb = (int32_t)(chunk % io.spi);
     asm volatile(

@@ -432,11 +432,13 @@ bool build_pass(PassPlan& p, int kind, int N, int64_t count, int64_t images, int
     p.in.images = images;
     p.in.C = T;
     p.in.spi = rows / T;
-    p.in.n_sub = 1;
-    p.in.sub_bytes = E * 4;
+    // (more than 256 blocks: boxes of 256 blocks each, consecutive in SMEM)
+    p.in.n_sub = (N / blk + 255) / 256;
+    p.in.sub_bytes = E * 4 / p.in.n_sub;
+    p.in.box_rows = (N / blk) / p.in.n_sub;  // blocks per box
     p.in.swz = 0;
     p.in.total = count * (int64_t)N;
-    if (N / blk > 256 || T * blk > 256 || rows % T) {
+    if ((N / blk) % p.in.n_sub || T * blk > 256 || rows % T) {
       if (err) *err = "blocked rows: unsupported geometry";
       return false;
     }
@@ -806,10 +808,17 @@ static int build_three_step(Plan& plan, int nx, int lg, int64_t batch, std::stri
 static int build_two_pass_blocked(Plan& plan, int nx, int lg, int64_t batch, std::string* err) {
   const int a = lg / 2, b = lg - a;
   const int N1 = 1 << a, N2 = 1 << b;
-  const int E1 = std::min(16384, 16 * N1), E2 = std::min(16384, 16 * N2);
+  // pass 1: 8192-element strips (two CTAs per SM) for N1 >= 1024 — more
+  // independent chunk chains per SM beat wider runs: 2^20 0.66 -> 0.74 of
+  // roofline with 8 instead of 16 columns (round 2)
+  // pass 2: 8192-element chunks for rows of <= 1024 (eight rows: 32-byte
+  // output runs, two CTAs per SM; 2^20 0.73 -> 0.79), 16384 for 2048 (eight
+  // rows; four rows would leave 16-byte runs: 0.29)
+  const int E1 = N1 >= 1024 ? 8192 : std::min(16384, 16 * N1);
+  const int E2 = N2 <= 1024 ? 8192 : std::min(16384, 16 * N2);
   PassPlan p1, p2;
   if (!build_pass(p1, kPassStrip, N1, 0, batch, N2, err, nx, 0, 0, E1)) return 6;
-  if (p1.IMG != 1 || p1.C * 4 < 32) {
+  if (p1.IMG != 1 || p1.C * 4 < 16) {
     if (err) *err = "unsupported two-pass geometry";
     return 6;
   }
@@ -818,7 +827,7 @@ static int build_two_pass_blocked(Plan& plan, int nx, int lg, int64_t batch, std
   // pass 2 reads the tiles with their swizzle (T-row groups of a block are
   // whole swizzle atoms, aligned alike in the workspace and in shared memory)
   p2.in.swz = p2.swz_in = p1.swz_out;
-  if ((p2.T * p1.C * 4) % (p1.C * 4 * 8) != 0) {
+  if (p1.swz_out && (p2.T * p1.C * 4) % (p1.C * 4 * 8) != 0) {
     if (err) *err = "two-pass: row group is not a whole swizzle atom";
     return 6;
   }

@@ -116,6 +116,9 @@ const KernelEntry kKernels[] = {
     // twiddled strips and blocked rows of 128 .. 512
     KENTRY(2048, 8, 16, 0, 4, 1, true), KENTRY(2048, 8, 16, 0, 4, 6, false), KENTRY(4096, 16, 16, 0, 4, 6, false),
     KENTRY(8192, 16, 32, 0, 2, 6, false),
+    // two-pass: 8192-element strips of 1024 rows (first pass); blocked rows of
+    // 1024 / 2048 in 8192-element chunks (experiment TCFFT_RCHUNK_<n>)
+    KENTRY(8192, 32, 32, 0, 2, 1, true), KENTRY(8192, 64, 32, 0, 2, 6, false), KENTRY(8192, 32, 32, 0, 2, 6, false),
     // column strips of 256 columns for N <= 8 (2D nx <= 8 with ny > 256)
     KSTRIP(512, 2, 0, 0, 4),      KSTRIP(1024, 4, 0, 0, 4),     KSTRIP(2048, 8, 0, 0, 4),
     // rows of 4 .. 16 whose element count is not a multiple of 32 (unswizzled staging)
@@ -251,7 +254,7 @@ tcfftResult make_tmap(CUtensorMap* tm, const tcfft::IoDesc& io, const void* base
     cuuint64_t dims[4] = {(cuuint64_t)g, (cuuint64_t)(io.rows / io.C), (cuuint64_t)io.cols, (cuuint64_t)io.images};
     cuuint64_t strides[3] = {(cuuint64_t)g * 4, (cuuint64_t)io.W * io.rows * 4,
                              (cuuint64_t)io.W * io.rows * io.cols * 4};
-    cuuint32_t box[4] = {(cuuint32_t)g, 1, (cuuint32_t)io.cols, 1};
+    cuuint32_t box[4] = {(cuuint32_t)g, 1, (cuuint32_t)(io.cols / io.n_sub), 1};
     cuuint32_t es[4] = {1, 1, 1, 1};
     r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, const_cast<void*>(base), dims, strides, box, es,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
