@@ -1054,6 +1054,7 @@ int build_plan_dist(Plan& plan, int nx, int rank, int world, std::string* err, b
   }
   plan.passes.push_back(std::move(p0));
   plan.passes.push_back(std::move(p1));
+  plan.dist = fused ? 2 : 1;
   return 0;
 }
 

@@ -130,6 +130,7 @@ struct Plan {
   int32_t nx = 0, ny = 0;
   int64_t batch = 0;
   size_t ws_bytes = 0;
+  int32_t dist = 0;         // distributed single-transform plan: 1 NCCL-exchange variant, 2 fused (peer stores)
   int64_t groups = 1;       // passes run once per group of transforms
   size_t group_bytes = 0;   // input / output bytes of one group
   std::vector<PassPlan> passes;

@@ -537,7 +537,7 @@ tcfftResult tcfftSetPassMask(tcfftHandle plan, unsigned mask) {
 
 tcfftResult tcfftExecC2C(tcfftHandle plan, const void* idata, void* odata) {
   if (!valid(plan)) return TCFFT_INVALID_PLAN;
-  if (!idata || !odata || !on_plan_device(plan)) return TCFFT_INVALID_VALUE;
+  if (!idata || !odata || !on_plan_device(plan) || plan->plan.dist) return TCFFT_INVALID_VALUE;
   if ((reinterpret_cast<uintptr_t>(idata) | reinterpret_cast<uintptr_t>(odata)) & 15) return TCFFT_INVALID_VALUE;
   if (plan->plan.groups > 1 && plan->pass_mask == ~0u) return exec_grouped(plan, idata, odata);
   return launch_passes(plan, idata, odata, plan->stream);
@@ -691,6 +691,7 @@ static tcfftResult build_pipe(tcfftHandle plan) {
 
 extern "C" tcfftResult tcfftExecC2CHost(tcfftHandle plan, const void* hin, void* hout) {
   if (!valid(plan)) return TCFFT_INVALID_PLAN;
+  if (plan->plan.dist) return TCFFT_INVALID_VALUE;  // distributed plans: tcfftExecDistPass
   if (!hin || !hout || !on_plan_device(plan)) return TCFFT_INVALID_VALUE;
   if (!plan->pipe) {
     tcfftResult st = build_pipe(plan);
@@ -760,6 +761,7 @@ __global__ void strided_copy_kernel(const uint32_t* __restrict__ src, uint32_t* 
 extern "C" tcfftResult tcfftExecC2CStrided(tcfftHandle plan, const void* idata, void* odata, long long stride,
                                            long long batch_stride) {
   if (!valid(plan)) return TCFFT_INVALID_PLAN;
+  if (plan->plan.dist) return TCFFT_INVALID_VALUE;  // distributed plans: tcfftExecDistPass
   if (!idata || !odata || !on_plan_device(plan)) return TCFFT_INVALID_VALUE;
   const tcfft::Plan& P = plan->plan;
   const int64_t n = (int64_t)P.nx * (P.dims == 2 ? P.ny : 1);
@@ -943,7 +945,7 @@ tcfftResult tcfftPlan1DDistFused(tcfftHandle* plan, int nx, int rank, int world)
 
 tcfftResult tcfftDistSetPeers(tcfftHandle plan, const void* const* recv, int world) {
   if (!valid(plan)) return TCFFT_INVALID_PLAN;
-  if (plan->dev.empty() || plan->plan.passes[0].out.mode != tcfft::kIoPeer || !recv ||
+  if (plan->plan.dist != 2 || plan->plan.passes[0].out.mode != tcfft::kIoPeer || !recv ||
       world != plan->plan.passes[0].out.npeer)
     return TCFFT_INVALID_VALUE;
   for (int h = 0; h < world; ++h) {
@@ -995,7 +997,7 @@ tcfftResult tcfftDistPlanTablesFused(int nx, int rank, int world, int pass, void
 
 tcfftResult tcfftExecDistPass(tcfftHandle plan, int pass, const void* idata, void* odata) {
   if (!valid(plan)) return TCFFT_INVALID_PLAN;
-  if (pass < 0 || pass >= (int)plan->dev.size() || plan->plan.ws_bytes) return TCFFT_INVALID_VALUE;
+  if (!plan->plan.dist || pass < 0 || pass >= (int)plan->dev.size()) return TCFFT_INVALID_VALUE;
   if (!idata || !odata || !on_plan_device(plan)) return TCFFT_INVALID_VALUE;
   if ((reinterpret_cast<uintptr_t>(idata) | reinterpret_cast<uintptr_t>(odata)) & 15) return TCFFT_INVALID_VALUE;
   const PassPlan& p = plan->plan.passes[pass];
@@ -1014,7 +1016,7 @@ tcfftResult tcfftExecDistPass(tcfftHandle plan, int pass, const void* idata, voi
 
 tcfftResult tcfftDistUnpack(tcfftHandle plan, int world, const void* recv, void* rows) {
   if (!valid(plan)) return TCFFT_INVALID_PLAN;
-  if (plan->plan.passes.size() != 2 || world < 1 || !recv || !rows || !on_plan_device(plan)) return TCFFT_INVALID_VALUE;
+  if (plan->plan.dist != 1 || world < 1 || !recv || !rows || !on_plan_device(plan)) return TCFFT_INVALID_VALUE;
   const PassPlan& p1 = plan->plan.passes[1];
   // received [G][N1/G][N2/G] (block h from rank h = columns h N2/G ..) -> rows [N1/G][N2]
   const int64_t N2 = p1.N, nrows = p1.count;

@@ -169,3 +169,26 @@ def test_dist_transform_two_ranks_one_gpu(nx, fused):
     assert R.rel_l2(got, R.fft64(x, nx)[0]) < 1.5e-3
     if nx <= 1 << 16:
         assert R.rel_l2(got, R.to_complex(R.fft_half(x))[0]) < 2e-3
+
+
+@pytest.mark.gpu
+def test_dist_plan_rejects_regular_exec():
+    """A distributed plan's passes only run through tcfftExecDistPass; the
+    single-GPU entry points and the wrong variant's calls are refused."""
+    import ctypes
+
+    L = _lib.load()
+    for fused in (False, True):
+        h = ctypes.c_void_p()
+        make = L.tcfftPlan1DDistFused if fused else L.tcfftPlan1DDist
+        assert make(ctypes.byref(h), 1 << 16, 0, 2) == 0
+        buf = torch.empty((1 << 16, 2), dtype=torch.float16, device="cuda")
+        ptr = ctypes.c_void_p(buf.data_ptr())
+        assert L.tcfftExecC2C(h, ptr, ptr) == 3  # TCFFT_INVALID_VALUE
+        if fused:
+            assert L.tcfftDistUnpack(h, 2, ptr, ptr) == 3
+            assert L.tcfftExecDistPass(h, 0, ptr, ptr) == 3  # peers not set yet
+        else:
+            arr = (ctypes.c_void_p * 2)(buf.data_ptr(), buf.data_ptr())
+            assert L.tcfftDistSetPeers(h, arr, 2) == 3
+        assert L.tcfftDestroy(h) == 0
