@@ -537,10 +537,17 @@ bool build_pass(PassPlan& p, int kind, int N, int64_t count, int64_t images, int
     // a row of the strip is 4 words): the radix-64 writer's 16-byte stores of
     // a quarter-warp then cover 128 contiguous bytes.
     const bool quarter = !row_in && C == 4 && strip_quarter_order();
+    // Blocked-row inputs: the rows of a butterfly fastest (key n T + tr).  A
+    // warp still covers every (row, n % Bw) bank of its block group for the
+    // gather, and a quarter-warp (8 rows of one butterfly) stores the radix-64
+    // writer's vectors to 8 consecutive padded row blocks (staging-address
+    // order put 2 rows x 4 butterflies there: 2-way conflicts at Bw = 4)
+    const char* ebo = experiment_env("TCFFT_BLK_ORDER");  // experiment: 0 = staging-address order
+    const bool rows_fast = blk_in && (!ebo || std::atoi(ebo) != 0);
     for (int tr = 0; tr < T; ++tr)
       for (int blk = 0; blk < N / R1; ++blk) {
         const int n = bnat(blk);
-        const int32_t key = quarter ? (((n / 8) * C + tr) * 8 + n % 8) : w_in(tr, n);
+        const int32_t key = rows_fast ? n * T + tr : quarter ? (((n / 8) * C + tr) * 8 + n % 8) : w_in(tr, n);
         order.emplace_back(key, tr, blk);
       }
     std::sort(order.begin(), order.end());

@@ -69,11 +69,7 @@ def test_bank_conflicts_report(capsys):
                 # TMA-stored tile, plan.cpp pitch_pad_words_out).  (The radix-64 / 32
                 # writers of 8- / 16-column strips were 2-way with 4 writer groups:
                 # 8 groups since round 2, plan.cpp writer_groups)
-                # and the blocked-rows pass of 2048-point rows fed by 4-column first-pass
-                # strips (2^22: the writer or the gather conflicts with 4-word blocks;
-                # the 8192-element first pass that needs them is worth it, round 2)
-                known = (d["kind"] in ("row", "stripT") or (d["kind"] == "rowT" and d["N"] == 256)
-                         or (d["kind"] == "rowTB" and d["N"] == 2048 and d["W"] == 4))
+                known = d["kind"] in ("row", "stripT") or (d["kind"] == "rowT" and d["N"] == 256)
                 assert r <= (2.0 if known else 1.0), (dims, nx, ny, pi, k, r)
     with capsys.disabled():
         print("\n" + "\n".join(lines))
