@@ -74,3 +74,36 @@ def test_bench_two_ranks_strong_scaling_json():
     assert d["n_gpus"] == 2 and d["scaling"] == "strong"
     assert d["config"]["batch"] == 16384 and d["config"]["batch_per_gpu"] == 8192
     assert d["value"] > 0 and d["gpu_launches"] == d["steps"]
+
+
+@pytest.mark.gpu
+def test_sweep_one_size_json_with_cpu_baseline_and_clocks():
+    """scripts/sweep.py (C5): one JSON line per size with the burst and
+    sustained device figures, the clock record and the per-size CPU baseline."""
+    cmd = [sys.executable, str(ROOT / "scripts" / "sweep.py"), "--dims", "1", "--sizes", "10", "--reps", "3"]
+    res = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert res.returncode == 0, res.stderr[-3000:]
+    d = json.loads([l for l in res.stdout.splitlines() if l.startswith("{")][0])
+    assert d["nx"] == 1024 and d["n_gpus"] == 1 and d["batch"] == (1 << 27) // 1024
+    assert d["gflops_5nlogn"] > 0 and d["sustained"]["gflops_5nlogn"] > 0 and d["sustained"]["bursts"] >= 3
+    assert d["clocks"] is None or "sm_mhz" in d["clocks"]
+    cb = d["cpu_baseline"]
+    assert cb["kind"] == "port" and cb["cores"] >= 1 and cb["value"] > 0
+
+
+@pytest.mark.gpu
+def test_sweep_two_ranks_strong_scaling_json():
+    """scripts/sweep.py under torchrun with 2 ranks (gloo timing collectives,
+    both ranks on the one GPU): strong scaling shards each size's batch."""
+    env = dict(os.environ, TCFFT_BENCH_BACKEND="gloo", MASTER_ADDR="127.0.0.1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", "29519", str(ROOT / "scripts" / "sweep.py"),
+           "--dims", "2", "--sizes", "8", "--reps", "3", "--no-cpu"]
+    res = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
+    assert res.returncode == 0, res.stderr[-3000:]
+    lines = [l for l in res.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, res.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["scaling"] == "strong"
+    assert d["batch"] == (1 << 27) // 65536 and d["batch_per_gpu"] == d["batch"] // 2
+    assert "cpu_baseline" not in d
