@@ -743,6 +743,13 @@ extern "C" tcfftResult tcfftExecC2CHost(tcfftHandle plan, const void* hin, void*
 //   stride 1, batch_stride == N          : contiguous fast path
 //   stride 1, padded batch_stride (x4)   : per-transform bulk copies straight
 //                                          from the padded rows (64 <= N <= 1024)
+//   stride 1, batch_stride (x4), swizzled
+//   row plans (N = 32, 2048 .. 8192, and
+//   64 .. 256 in 4096-element chunks)     : a 3D tensor map {32, N/32, batch}
+//                                          whose batch stride is the view's:
+//                                          one TMA box per chunk, the same
+//                                          128B-swizzled staging image as the
+//                                          contiguous map (no extra HBM pass)
 //   anything else                        : gather into a contiguous scratch,
 //                                          transform, scatter back
 __global__ void strided_copy_kernel(const uint32_t* __restrict__ src, uint32_t* __restrict__ dst, int64_t batch,
@@ -782,6 +789,38 @@ extern "C" tcfftResult tcfftExecC2CStrided(tcfftHandle plan, const void* idata, 
     kp.in.gstride_bytes = kp.out.gstride_bytes = batch_stride * 4;
     if (kp.ctr) kp.ctr += 2 * (__atomic_fetch_add(&d.launches, 1u, __ATOMIC_RELAXED) % kTicketSlots);
     d.k->launch(dim3(d.grid), p.smem_bytes, plan->stream, t0, t1, kp);
+    return cudaGetLastError() == cudaSuccess ? TCFFT_SUCCESS : TCFFT_EXEC_FAILED;
+  }
+  if (P.dims == 1 && stride == 1 && (batch_stride % 4) == 0 && plan->dev.size() == 1 &&
+      P.passes[0].kind == tcfft::kPassRow && P.passes[0].in.W == 32 &&
+      (P.passes[0].in.mode == tcfft::kIoFlat || P.passes[0].in.mode == tcfft::kIoFlat3) && P.nx % 32 == 0 &&
+      P.nx / 32 <= 256 && P.passes[0].T <= 256) {
+    const PassPlan& p = P.passes[0];
+    const DevPass& d = plan->dev[0];
+    auto enc = encode_fn();
+    if (!enc) return TCFFT_EXEC_FAILED;
+    CUtensorMap tm[2];
+    const void* ptr[2] = {idata, odata};
+    for (int i = 0; i < 2; ++i) {
+      std::memset(&tm[i], 0, sizeof(tm[i]));
+      cuuint64_t dims[3] = {32, (cuuint64_t)(P.nx / 32), (cuuint64_t)P.batch};
+      cuuint64_t strides[2] = {128, (cuuint64_t)batch_stride * 4};
+      cuuint32_t box[3] = {32, (cuuint32_t)(P.nx / 32), (cuuint32_t)p.T};
+      cuuint32_t es[3] = {1, 1, 1};
+      if (enc(&tm[i], CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, const_cast<void*>(ptr[i]), dims, strides, box, es,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return TCFFT_EXEC_FAILED;
+    }
+    // kernel kIoFlat3: box {32, N/32, T} at {0, 0, chunk * T} (T transforms of N * 4 bytes)
+    KParams kp = d.kp;
+    for (tcfft::KIo* io : {&kp.in, &kp.out}) {
+      io->mode = tcfft::kIoFlat3;
+      io->n_sub = p.T;
+      io->sub_bytes = P.nx * 4;
+    }
+    if (kp.ctr) kp.ctr += 2 * (__atomic_fetch_add(&d.launches, 1u, __ATOMIC_RELAXED) % kTicketSlots);
+    d.k->launch(dim3(d.grid), p.smem_bytes, plan->stream, tm[0], tm[1], kp);
     return cudaGetLastError() == cudaSuccess ? TCFFT_SUCCESS : TCFFT_EXEC_FAILED;
   }
   // general view: gather -> contiguous transform -> scatter

@@ -49,7 +49,10 @@ def _strided_case(n, batch, stride, bstride, seed):
 @pytest.mark.gpu
 @pytest.mark.parametrize("n,batch,stride,bstride", [(256, 8, 1, 256), (256, 8, 1, 260), (1024, 3, 1, 1100),
                                                       (512, 4, 3, 2000), (4, 2, 8, 32), (4096, 4, 2, 8195),
-                                                      (1 << 15, 2, 1, (1 << 15) + 16)])
+                                                      (1 << 15, 2, 1, (1 << 15) + 16),
+                                                      # row-pitched 3D tensor maps (swizzled row plans):
+                                                      (4096, 5, 1, 4100), (2048, 7, 1, 2052), (8192, 3, 1, 8200),
+                                                      (32, 300, 1, 36), (256, 10001, 1, 260), (4096, 3, 1, 4098)])
 def test_strided_views_equal_contiguous(n, batch, stride, bstride):
     x, buf, idx = _strided_case(n, batch, stride, bstride, 3)
     t = torch.from_numpy(buf).cuda()
