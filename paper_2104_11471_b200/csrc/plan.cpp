@@ -153,6 +153,22 @@ std::vector<int> choose_radices(int n, int kind, bool twiddled) {
     const char* e3 = experiment_env("TCFFT_STRIP128");
     if (!e3 || std::atoi(e3) != 0) return {8, 16};
   }
+  // experiment hook: TCFFT_RADICES_<n>=a,b[,c] overrides a row pass's radix list
+  // (needs a matching kernel instantiation; the 16384 / 8192 alternatives were
+  // measured no better, profiles/exp_radix_r02.txt)
+  if (kind == kPassRow) {
+    char key[40];
+    std::snprintf(key, sizeof(key), "TCFFT_RADICES_%d", n);
+    if (const char* ev = experiment_env(key)) {
+      std::vector<int> r;
+      for (const char* q = ev; *q;) {
+        r.push_back(std::atoi(q));
+        while (*q && *q != ',') ++q;
+        if (*q == ',') ++q;
+      }
+      return r;
+    }
+  }
   // (2D column strips 1024^2: 0.75 -> 0.83 of roofline)
   if (kind == kPassStrip && !twiddled && (n == 512 || n == 1024)) {
     const char* e2 = experiment_env("TCFFT_STRIP_R64");
