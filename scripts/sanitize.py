@@ -39,7 +39,11 @@ def run(nx, ny, batch, oop=False):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--quick", action="store_true")
+    ap.add_argument("--views", action="store_true", help="only the strided-view cases")
     a = ap.parse_args()
+    if a.views:
+        views()
+        return
     cases = [(n, None, b) for n, b in [(2, 1024), (4, 512), (4, 3), (8, 257), (16, 33), (32, 64), (64, 64),
                                         (128, 40), (256, 16), (256, 4096), (512, 24), (1024, 12), (1024, 200),
                                         (2048, 8), (4096, 4), (4096, 4096), (8192, 4), (16384, 4)]]
@@ -68,14 +72,21 @@ def main():
     plan = tc.plan_1d(4096, 2048)
     h = (torch.rand((2048, 4096, 2)) * 2 - 1).half().pin_memory()
     tc.execute_host(plan, h)
+    views()
+    print("sanitize cases done", flush=True)
+
+
+def views():
+    # general view (gather / scatter), padded-pitch bulk copies, row-pitched
+    # 3D tensor maps (full and partial last chunk)
     wide = torch.zeros((8, 2 * 4096, 2), device="cuda", dtype=torch.float16)
     v = tc.BatchedTensor(wide.view(-1, 2), 8, 4096, stride=2, batch_stride=2 * 4096)
     tc.execute(tc.plan_1d(4096, 8), v)
-    pv = tc.BatchedTensor(torch.zeros((4 * 1100, 2), device="cuda", dtype=torch.float16), 4, 1024,
-                          batch_stride=1100)
-    tc.execute(tc.plan_1d(1024, 4), pv)
-    torch.cuda.synchronize()
-    print("sanitize cases done", flush=True)
+    for n, b, bs in ((1024, 4, 1100), (4096, 5, 4100), (32, 300, 36), (256, 10001, 260), (8192, 3, 8200)):
+        pv = tc.BatchedTensor((torch.rand((b * bs, 2), device="cuda") * 2 - 1).half(), b, n, batch_stride=bs)
+        tc.execute(tc.plan_1d(n, b), pv)
+        torch.cuda.synchronize()
+        print("ok view", n, b, bs, flush=True)
 
 
 if __name__ == "__main__":
