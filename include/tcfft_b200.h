@@ -72,8 +72,10 @@ tcfftResult tcfftExecC2C(tcfftHandle plan, const void* idata, void* odata);
 tcfftResult tcfftExecC2CHost(tcfftHandle plan, const void* hin, void* hout);
 /* Strided views (reference BatchedTensor, executor.py:25-51): element j of
  * transform b at idata[b*batch_stride + j*stride] (complex elements), same for
- * odata; 2D plans require stride 1.  Contiguous and padded-row views run the
- * transform directly; other views go through a plan-owned contiguous scratch. */
+ * odata; 2D plans require stride 1.  Contiguous views and row-pitched 1D
+ * views (stride 1, batch_stride a multiple of 4: one-pass plans and the
+ * two-pass plans of 2^15 .. 2^22) run the transform directly on the view;
+ * other views go through a plan-owned contiguous scratch. */
 tcfftResult tcfftExecC2CStrided(tcfftHandle plan, const void* idata, void* odata, long long stride,
                                 long long batch_stride);
 tcfftResult tcfftDestroy(tcfftHandle plan);

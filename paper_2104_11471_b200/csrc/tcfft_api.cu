@@ -263,7 +263,7 @@ tcfftResult make_tmap(CUtensorMap* tm, const tcfft::IoDesc& io, const void* base
     const int k = io.rows / 256;
     cuuint64_t dims[4] = {(cuuint64_t)io.cols, 256, (cuuint64_t)k, (cuuint64_t)io.images};
     cuuint64_t strides[3] = {(cuuint64_t)io.cols * 4, (cuuint64_t)io.cols * 256 * 4,
-                             (cuuint64_t)io.cols * io.rows * 4};
+                             (cuuint64_t)(io.img_stride ? io.img_stride : (int64_t)io.cols * io.rows) * 4};
     cuuint32_t box[4] = {(cuuint32_t)io.C, 256, (cuuint32_t)k, 1};
     cuuint32_t es[4] = {1, 1, 1, 1};
     const int run = io.C * 4;
@@ -508,7 +508,10 @@ bool on_plan_device(tcfftHandle h) {
 
 }  // namespace
 
-static tcfftResult launch_passes(tcfftHandle plan, const void* idata, void* odata, cudaStream_t st);
+// bstride > 0: row-pitched batch (strided views): the first pass reads and the
+// last pass writes image b at b * bstride elements (box tensor maps)
+static tcfftResult launch_passes(tcfftHandle plan, const void* idata, void* odata, cudaStream_t st,
+                                 int64_t bstride = 0);
 static tcfftResult exec_grouped(tcfftHandle plan, const void* idata, void* odata);
 
 extern "C" {
@@ -546,7 +549,7 @@ tcfftResult tcfftExecC2C(tcfftHandle plan, const void* idata, void* odata) {
 }  // extern "C"
 
 // All pass launches of one execution, on stream `st`.
-static tcfftResult launch_passes(tcfftHandle plan, const void* idata, void* odata, cudaStream_t st) {
+static tcfftResult launch_passes(tcfftHandle plan, const void* idata, void* odata, cudaStream_t st, int64_t bstride) {
   for (int64_t g = 0; g < plan->plan.groups; ++g) {
   const size_t goff = (size_t)g * plan->plan.group_bytes;
   const void* src = static_cast<const char*>(idata) + goff;
@@ -560,7 +563,10 @@ static tcfftResult launch_passes(tcfftHandle plan, const void* idata, void* odat
       continue;
     }
     CUtensorMap tin, tout;
-    if (make_tmap(&tin, p.in, src) != TCFFT_SUCCESS || make_tmap(&tout, p.out, dst) != TCFFT_SUCCESS)
+    tcfft::IoDesc din = p.in, dout = p.out;
+    if (bstride && i == 0) din.img_stride = bstride;
+    if (bstride && i + 1 == plan->dev.size()) dout.img_stride = bstride;
+    if (make_tmap(&tin, din, src) != TCFFT_SUCCESS || make_tmap(&tout, dout, dst) != TCFFT_SUCCESS)
       return TCFFT_EXEC_FAILED;
     KParams kp = d.kp;
     kp.in.gptr = static_cast<const uint8_t*>(src);
@@ -822,6 +828,18 @@ extern "C" tcfftResult tcfftExecC2CStrided(tcfftHandle plan, const void* idata, 
     if (kp.ctr) kp.ctr += 2 * (__atomic_fetch_add(&d.launches, 1u, __ATOMIC_RELAXED) % kTicketSlots);
     d.k->launch(dim3(d.grid), p.smem_bytes, plan->stream, tm[0], tm[1], kp);
     return cudaGetLastError() == cudaSuccess ? TCFFT_SUCCESS : TCFFT_EXEC_FAILED;
+  }
+  // two-pass plans (1D 2^15 .. 2^22) whose first pass reads and last pass
+  // writes the user buffer through box tensor maps with one image per
+  // transform: the image stride becomes the view's batch stride
+  if (P.dims == 1 && stride == 1 && (batch_stride % 4) == 0 && P.groups == 1 && P.passes.size() == 2 &&
+      P.passes[0].ws_out && P.passes[1].ws_in && plan->pass_mask == ~0u) {
+    auto boxed = [&](const tcfft::IoDesc& io) {
+      return (io.mode == tcfft::kIoBox || io.mode == tcfft::kIoBoxR) && io.images == P.batch && !io.img_split &&
+             !io.img_stride && (int64_t)io.rows * io.cols == n;
+    };
+    if (boxed(P.passes[0].in) && boxed(P.passes[1].out))
+      return launch_passes(plan, idata, odata, plan->stream, batch_stride);
   }
   // general view: gather -> contiguous transform -> scatter
   const size_t bytes = (size_t)(P.batch * n * 4);

@@ -2,7 +2,8 @@
 transform on a contiguous batch, on a row-pitched view (batch_stride = N + 4:
 row-pitched tensor maps / padded-pitch bulk copies, one HBM pass) and on a
 general view (stride 2: gather -> transform -> scatter).  One JSON line per
-case: ms and the HBM fraction at 8 B per element per pass.
+case: ms and the HBM fraction of the FFT's own passes (8 B per element per
+pass; the general view's gather / scatter copies come on top).
 
     python scripts/strided_probe.py
 """
@@ -34,7 +35,7 @@ def timed(fn, reps=10):
 
 def main():
     peak, _ = bench._peaks()
-    for n, batch in ((4096, 16384), (2048, 32768), (256, 262144), (1024, 65536)):
+    for n, batch in ((4096, 16384), (2048, 32768), (256, 262144), (1024, 65536), (1 << 16, 1024), (1 << 22, 16)):
         plan = tc.plan_1d(n, batch)
         for name, stride, bstride in (("contiguous", 1, n), ("row-pitched", 1, n + 4), ("general", 2, 2 * n + 4)):
             total = bstride * (batch - 1) + stride * (n - 1) + 1
@@ -44,10 +45,10 @@ def main():
             else:
                 v = tc.BatchedTensor(t, batch, n, stride=stride, batch_stride=bstride)
                 ms = timed(lambda: tc.execute(plan, v))
-            gbs = batch * n * 8 / (ms * 1e-3) / 1e9
+            gbs = batch * n * 8 * len(plan.passes) / (ms * 1e-3) / 1e9
             print(json.dumps({"n": n, "batch": batch, "view": name, "stride": stride, "batch_stride": bstride,
-                              "ms": round(ms, 4), "hbm_gbs_1pass": round(gbs, 1),
-                              "frac_1pass": round(gbs / peak, 3)}), flush=True)
+                              "passes": len(plan.passes), "ms": round(ms, 4),
+                              "hbm_gbs_fft_passes": round(gbs, 1), "frac": round(gbs / peak, 3)}), flush=True)
             del t
 
 

@@ -52,7 +52,10 @@ def _strided_case(n, batch, stride, bstride, seed):
                                                       (1 << 15, 2, 1, (1 << 15) + 16),
                                                       # row-pitched 3D tensor maps (swizzled row plans):
                                                       (4096, 5, 1, 4100), (2048, 7, 1, 2052), (8192, 3, 1, 8200),
-                                                      (32, 300, 1, 36), (256, 10001, 1, 260), (4096, 3, 1, 4098)])
+                                                      (32, 300, 1, 36), (256, 10001, 1, 260), (4096, 3, 1, 4098),
+                                                      # two-pass plans, box tensor maps at the view's image stride:
+                                                      (1 << 16, 3, 1, (1 << 16) + 4), (1 << 18, 2, 1, (1 << 18) + 256),
+                                                      (1 << 20, 2, 1, (1 << 20) + 64), (1 << 22, 2, 1, (1 << 22) + 8)])
 def test_strided_views_equal_contiguous(n, batch, stride, bstride):
     x, buf, idx = _strided_case(n, batch, stride, bstride, 3)
     t = torch.from_numpy(buf).cuda()
