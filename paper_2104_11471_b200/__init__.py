@@ -21,6 +21,8 @@ import threading
 from dataclasses import dataclass, field
 from functools import reduce
 
+import numpy as np
+
 from . import _lib
 
 __version__ = "0.1.0"
@@ -232,6 +234,10 @@ def execute(plan: Plan, data, out=None, stream=None):
         raise ExecuteError("plan has been destroyed")
     from .tensor import BatchedTensor
 
+    if _is_host_view(data):
+        return _execute_host_view(plan, data, stream)
+    if isinstance(data, np.ndarray):
+        raise ExecuteError("host numpy data: pass a BatchedTensor view of it (the reference API) or use execute_host")
     if isinstance(data, BatchedTensor):
         return _execute_view(plan, data, stream)
     t, n = _as_pairs(data)
@@ -256,6 +262,44 @@ def execute(plan: Plan, data, out=None, stream=None):
     if st != _lib.TCFFT_SUCCESS:
         raise ExecuteError(f"tcfftExecC2C failed: {_lib.error_string(st)}")
     return o if out is not None else data
+
+
+def _is_host_view(data) -> bool:
+    """A BatchedTensor-shaped object over a host numpy buffer: ours, or the
+    reference's own ``tcfft.BatchedTensor`` (executor.py:25-74)."""
+    return all(hasattr(data, a) for a in ("pairs", "batch", "length", "stride", "batch_stride")) and \
+        isinstance(data.pairs, np.ndarray)
+
+
+def _execute_host_view(plan: Plan, data, stream=None):
+    """Reference-style execute on host data (executor.py:152-190): the view's
+    numpy buffer is transformed in place.  Contiguous batches go through the
+    pipelined host-buffer path (tcfftExecC2CHost); other views copy the
+    buffer to the plan's device, run the strided device path and copy back
+    (the device path leaves elements outside the view untouched)."""
+    import torch
+
+    p = data.pairs
+    if p.dtype != np.float16:
+        raise ExecuteError(f"plan precision half needs {np.dtype(np.float16)} storage, got {p.dtype}")
+    if p.ndim != 2 or p.shape[1] != 2:
+        raise ExecuteError(f"pairs must be (total, 2), got {p.shape}")
+    if data.length != plan.n_logical or data.batch != plan.batch:
+        raise ExecuteError(f"data shape (batch={data.batch}, len={data.length}) does not match plan "
+                           f"(batch={plan.batch}, len={plan.n_logical})")
+    if plan.dims == 2 and data.stride != 1:
+        raise ExecuteError("2D execution requires contiguous row-major data")
+    n = data.batch * data.length
+    if data.stride == 1 and (data.batch == 1 or data.batch_stride == data.length) and p.flags.c_contiguous:
+        execute_host(plan, torch.from_numpy(p[:n]), stream=stream)
+        return data
+    dev = torch.device("cuda", plan._device if plan._device >= 0 else torch.cuda.current_device())
+    d = torch.from_numpy(np.ascontiguousarray(p)).to(dev)
+    from .tensor import BatchedTensor
+
+    _execute_view(plan, BatchedTensor(d, data.batch, data.length, data.stride, data.batch_stride), stream)
+    np.copyto(p, d.cpu().numpy())  # (synchronises)
+    return data
 
 
 def _execute_view(plan: Plan, data, stream=None):

@@ -2,10 +2,14 @@
 (reference ``pkg/src/tcfft/executor.py:25-74``).
 
 Logical element j of sequence b lives at ``pairs[b*batch_stride + j*stride]``;
-``pairs`` is a ``(total, 2)`` float16 CUDA tensor with re at ``[..., 0]``.
-``execute(plan, BatchedTensor)`` transforms the view in place through
-``tcfftExecC2CStrided`` (contiguous and padded-row views run directly, other
-views via a plan-owned contiguous scratch).
+``pairs`` is a ``(total, 2)`` float16 array with re at ``[..., 0]``: a CUDA
+tensor (device view), or, as in the reference, a host numpy array.
+``execute(plan, BatchedTensor)`` transforms the view in place: device views
+through ``tcfftExecC2CStrided`` (contiguous and row-pitched views run directly,
+other views via a plan-owned contiguous scratch), host views through the
+host-buffer pipeline (``tcfftExecC2CHost``) or a device copy of the buffer.
+The reference's own ``BatchedTensor`` objects (numpy ``pairs``) are accepted
+by ``execute`` as they are.
 """
 
 from __future__ import annotations
@@ -19,7 +23,8 @@ class BatchedTensor:
     def __init__(self, pairs, batch: int, length: int, stride: int = 1, batch_stride: int | None = None):
         import torch
 
-        if not isinstance(pairs, torch.Tensor) or pairs.dim() != 2 or pairs.shape[1] != 2:
+        ok = (isinstance(pairs, torch.Tensor) and pairs.dim() == 2) or (isinstance(pairs, np.ndarray) and pairs.ndim == 2)
+        if not ok or pairs.shape[1] != 2:
             shape = tuple(pairs.shape) if hasattr(pairs, "shape") else type(pairs).__name__
             raise ExecuteError(f"pairs must be (total, 2), got {shape}")
         if batch_stride is None:
@@ -60,5 +65,6 @@ class BatchedTensor:
     def to_complex(self) -> np.ndarray:
         """Gather the logical (batch, length) sequences as complex128 (host)."""
         idx = self.offsets()[:, None] + np.arange(self.length) * self.stride
-        vals = self.pairs.detach().cpu().numpy()[idx]
+        p = self.pairs if isinstance(self.pairs, np.ndarray) else self.pairs.detach().cpu().numpy()
+        vals = p[idx]
         return vals[..., 0].astype(np.float64) + 1j * vals[..., 1].astype(np.float64)

@@ -77,3 +77,58 @@ def test_interleaved_view_aliases_like_reference():
     # (executor.py:45-46); interleaved columns are the 2D column pass instead
     with pytest.raises(tc.ExecuteError):
         tc.BatchedTensor(torch.zeros((64, 2), dtype=torch.float16), 4, 16, stride=4, batch_stride=1)
+
+
+def test_host_view_validation_cpu():
+    """numpy-backed views (the reference's BatchedTensor storage) are accepted
+    by the constructor and checked like the reference before any device work."""
+    v = tc.BatchedTensor(np.zeros((16, 2), np.float16), 2, 8)
+    assert v.offsets().tolist() == [0, 8] and v.to_complex().shape == (2, 8)
+    with pytest.raises(tc.ExecuteError):
+        tc.BatchedTensor(np.zeros((16, 3), np.float16), 2, 8)
+
+
+def _reference_batched_tensor_cls():
+    """The reference's own BatchedTensor class when its package is installed
+    (baseline/_ref, not on every box), else ours."""
+    import importlib
+    import sys
+    from pathlib import Path
+
+    ref = Path(__file__).resolve().parents[1] / "baseline" / "_ref"
+    if (ref / "tcfft").is_dir():
+        sys.path.insert(0, str(ref))
+        try:
+            return importlib.import_module("tcfft").BatchedTensor
+        except Exception:
+            pass
+        finally:
+            sys.path.remove(str(ref))
+    return tc.BatchedTensor
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,batch,stride,bstride", [(4096, 8, 1, 4096), (256, 8, 1, 260), (512, 4, 3, 2000),
+                                                      (1 << 16, 2, 1, 1 << 16), (64, 16, 2, 200)])
+def test_execute_on_host_views_like_reference(n, batch, stride, bstride):
+    """execute(plan, view) on a HOST numpy buffer, as a reference caller does
+    (executor.py:152-190): the reference's own BatchedTensor object when
+    available, transformed in place, nothing outside the view touched."""
+    BT = _reference_batched_tensor_cls()
+    x, buf, idx = _strided_case(n, batch, stride, bstride, 11)
+    view = BT(buf, batch, n, stride=stride, batch_stride=bstride)
+    out = tc.execute(tc.plan_1d(n, batch), view)
+    assert out is view
+    got = view.pairs
+    gates(got[idx], x, n)
+    mask = np.ones(len(buf), bool)
+    mask[idx.reshape(-1)] = False
+    assert np.all(got[mask] == np.float16(7.0))
+
+
+@pytest.mark.gpu
+def test_execute_host_view_rejects_wrong_dtype():
+    BT = _reference_batched_tensor_cls()
+    view = BT(np.zeros((64, 2), np.float64), 4, 16)
+    with pytest.raises(tc.ExecuteError):
+        tc.execute(tc.plan_1d(16, 4), view)
