@@ -35,9 +35,16 @@ def timed(fn, reps=10):
 
 def main():
     peak, _ = bench._peaks()
-    for n, batch in ((4096, 16384), (2048, 32768), (256, 262144), (1024, 65536), (1 << 16, 1024), (1 << 22, 16)):
-        plan = tc.plan_1d(n, batch)
-        for name, stride, bstride in (("contiguous", 1, n), ("row-pitched", 1, n + 4), ("general", 2, 2 * n + 4)):
+    cases = [((n, None), b) for n, b in ((4096, 16384), (2048, 32768), (256, 262144), (1024, 65536),
+                                          (1 << 16, 1024), (1 << 22, 16))]
+    cases += [((512, 512), 256), ((2048, 2048), 16)]
+    for (nx, ny), batch in cases:
+        n = nx * (ny or 1)
+        plan = tc.plan_1d(nx, batch) if ny is None else tc.plan_2d(nx, ny, batch)
+        views = (("contiguous", 1, n), ("row-pitched", 1, n + 4), ("general", 2, 2 * n + 4))
+        if ny:  # 2D: stride 1 only (executor.py:180-181); the general case is an unaligned pitch
+            views = (("contiguous", 1, n), ("row-pitched", 1, n + 4), ("general", 1, n + 2))
+        for name, stride, bstride in views:
             total = bstride * (batch - 1) + stride * (n - 1) + 1
             t = (torch.rand((total, 2), device="cuda") * 2 - 1).half()
             if name == "contiguous":
@@ -46,7 +53,7 @@ def main():
                 v = tc.BatchedTensor(t, batch, n, stride=stride, batch_stride=bstride)
                 ms = timed(lambda: tc.execute(plan, v))
             gbs = batch * n * 8 * len(plan.passes) / (ms * 1e-3) / 1e9
-            print(json.dumps({"n": n, "batch": batch, "view": name, "stride": stride, "batch_stride": bstride,
+            print(json.dumps({"nx": nx, "ny": ny, "batch": batch, "view": name, "stride": stride, "batch_stride": bstride,
                               "passes": len(plan.passes), "ms": round(ms, 4),
                               "hbm_gbs_fft_passes": round(gbs, 1), "frac": round(gbs / peak, 3)}), flush=True)
             del t

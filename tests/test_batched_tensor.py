@@ -132,3 +132,25 @@ def test_execute_host_view_rejects_wrong_dtype():
     view = BT(np.zeros((64, 2), np.float64), 4, 16)
     with pytest.raises(tc.ExecuteError):
         tc.execute(tc.plan_1d(16, 4), view)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("nx,ny,batch,bstride", [(512, 512, 3, 512 * 512 + 64), (256, 1024, 2, 256 * 1024 + 4),
+                                                  (1024, 4096, 2, 1024 * 4096 + 16), (64, 64, 5, 4100),
+                                                  (2048, 2048, 2, 2048 * 2048 + 32)])
+def test_2d_row_pitched_views(nx, ny, batch, bstride):
+    """2D batches at a padded image stride (executor.py:180-190 allows any
+    batch_stride with stride 1; gather -> transform -> scatter), against the
+    contiguous path and the oracle, nothing outside the view touched."""
+    n = nx * ny
+    x, buf, idx = _strided_case(n, batch, 1, bstride, 5)
+    t = torch.from_numpy(buf).cuda()
+    tc.execute(tc.plan_2d(nx, ny, batch), tc.BatchedTensor(t, batch, n, batch_stride=bstride))
+    got = t.cpu().numpy()
+    y = torch.from_numpy(np.ascontiguousarray(x)).cuda()
+    tc.execute(tc.plan_2d(nx, ny, batch), y)
+    assert np.array_equal(got[idx].view(np.uint16), y.cpu().numpy().view(np.uint16))
+    gates(got[idx][:2], x[:2], nx, ny)
+    mask = np.ones(len(buf), bool)
+    mask[idx.reshape(-1)] = False
+    assert np.all(got[mask] == np.float16(7.0))
