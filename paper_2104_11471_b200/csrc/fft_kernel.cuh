@@ -354,8 +354,29 @@ DEVI void final_epilogue(uint32_t taddr, uint32_t s_out, int obase, int ostride,
   }
 }
 
+// I/O modes a kernel MODE can meet (plan.cpp build_pass / the exec paths):
+// the branches of the others compile out of thread 0's load / store issue,
+// which sits on every chunk's critical path (two extra runtime branches there
+// measured -5% on C3, profiles/exp_views2d_r02.txt)
+template <int MODE>
+struct IoSet {
+  static constexpr uint32_t ROWS = (1u << kIoPitch) | (1u << kIoFlat) | (1u << kIoFlat3) | (1u << kIoRank1);
+  static constexpr uint32_t BOXES = (1u << kIoBox) | (1u << kIoBoxR);
+  static constexpr bool ROWK = MODE == kModeRow || MODE == kModeRowU;
+  static constexpr uint32_t IN = MODE == kModeRowTB ? (1u << kIoBlk) : (ROWK || MODE == kModeRowT) ? ROWS : ~0u;
+  static constexpr uint32_t OUT = (MODE == kModeRowTB || MODE == kModeRowT) ? BOXES : ROWK ? ROWS : ~0u;
+};
+// io.mode == M, decided at compile time when SET excludes M or holds only M
+template <uint32_t SET, int M>
+DEVI bool io_is(const KIo& io) {
+  if constexpr (!((SET >> M) & 1u)) return false;
+  else if constexpr (SET == (1u << M)) return true;
+  else return io.mode == M;
+}
+
+template <uint32_t SET>
 DEVI void issue_load(const CUtensorMap* tm, const KIo& io, int T, int64_t chunk, uint8_t* dst, uint64_t* bar) {
-  if (io.mode == kIoPitch) {
+  if (io_is<SET, kIoPitch>(io)) {
     const int64_t t0 = chunk * T;
     const int nt = (int)min((int64_t)T, io.count - t0);
     mbar_arrive_expect_tx(bar, (uint32_t)(nt * io.sub_bytes));
@@ -364,13 +385,13 @@ DEVI void issue_load(const CUtensorMap* tm, const KIo& io, int T, int64_t chunk,
     return;
   }
   mbar_arrive_expect_tx(bar, (uint32_t)(io.n_sub * io.sub_bytes));
-  if (io.mode == kIoFlat3) {  // whole > 256-row flat chunk in one 3D box
+  if (io_is<SET, kIoFlat3>(io)) {  // whole > 256-row flat chunk in one 3D box
     asm volatile(
         "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
         "[%5];" ::"r"(smem_u32(dst)),
         "l"(tm), "r"(0), "r"(0), "r"((int32_t)(chunk * io.n_sub)), "r"(smem_u32(bar))
         : "memory");
-  } else if (io.mode == kIoBlk) {  // C-row group rb of every Bw-wide block of one image, 4D boxes of <= 256 blocks
+  } else if (io_is<SET, kIoBlk>(io)) {  // C-row group rb of every Bw-wide block of one image, 4D boxes of <= 256 blocks
     const int32_t img = (int32_t)(chunk / io.spi), rb = (int32_t)(chunk % io.spi);
     const int32_t bpb = io.box_rows;  // blocks per box
     for (int i = 0; i < io.n_sub; ++i)
@@ -379,17 +400,17 @@ DEVI void issue_load(const CUtensorMap* tm, const KIo& io, int T, int64_t chunk,
           "%5}], [%6];" ::"r"(smem_u32(dst + i * io.sub_bytes)),
           "l"(tm), "r"(0), "r"(rb), "r"(i * bpb), "r"(img), "r"(smem_u32(bar))
           : "memory");
-  } else if (io.mode == kIoBoxR) {  // whole > 256-row strip in one 4D box
+  } else if (io_is<SET, kIoBoxR>(io)) {  // whole > 256-row strip in one 4D box
     const int32_t img = (int32_t)(chunk / io.spi), cb = (int32_t)(chunk % io.spi);
     asm volatile(
         "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, "
         "%5}], [%6];" ::"r"(smem_u32(dst)),
         "l"(tm), "r"(cb * io.C), "r"(0), "r"(0), "r"(img), "r"(smem_u32(bar))
         : "memory");
-  } else if (io.mode == kIoRank1) {
+  } else if (io_is<SET, kIoRank1>(io)) {
     const int32_t e0 = (int32_t)(chunk * io.chunk_rows);
     for (int i = 0; i < io.n_sub; ++i) tma_load_1d(dst + i * io.sub_bytes, tm, e0 + i * io.box_rows, bar);
-  } else if (io.mode == kIoFlat) {
+  } else if (io_is<SET, kIoFlat>(io)) {
     const int32_t row0 = (int32_t)(chunk * io.chunk_rows);
     for (int i = 0; i < io.n_sub; ++i) tma_load_2d(dst + i * io.sub_bytes, tm, 0, row0 + i * io.box_rows, bar);
   } else {
@@ -404,35 +425,35 @@ DEVI void issue_load(const CUtensorMap* tm, const KIo& io, int T, int64_t chunk,
   }
 }
 
-template <bool D4 = false>
+template <uint32_t SET, bool D4 = false>
 DEVI void issue_store(const CUtensorMap* tm, const KIo& io, int T, int64_t chunk, const uint8_t* src) {
-  if (io.mode == kIoPitch) {
+  if (io_is<SET, kIoPitch>(io)) {
     const int64_t t0 = chunk * T;
     const int nt = (int)min((int64_t)T, io.count - t0);
     for (int i = 0; i < nt; ++i)
       bulk_s2g(const_cast<uint8_t*>(io.gptr) + (t0 + i) * io.gstride_bytes, src + i * io.pitch_bytes, io.sub_bytes);
-  } else if (io.mode == kIoLinear) {  // the staging tile byte for byte, one bulk copy
+  } else if (io_is<SET, kIoLinear>(io)) {  // the staging tile byte for byte, one bulk copy
     bulk_s2g(const_cast<uint8_t*>(io.gptr) + chunk * (int64_t)io.sub_bytes, src, io.sub_bytes);
-  } else if (io.mode == kIoPeer) {
+  } else if (io_is<SET, kIoPeer>(io)) {
     // distributed plans: row slice h of the tile straight into rank h's
     // receive buffer (over NVLink for a peer GPU), at this chunk's global
     // column block: the exchange is the pass's own store
     const int64_t blk = io.peer_blk0 + chunk;
     for (int h = 0; h < io.npeer; ++h)
       bulk_s2g(const_cast<uint8_t*>(io.peers[h]) + blk * io.sub_bytes, src + h * io.sub_bytes, io.sub_bytes);
-  } else if (io.mode == kIoFlat3) {
+  } else if (io_is<SET, kIoFlat3>(io)) {
     asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(tm),
                  "r"(0), "r"(0), "r"((int32_t)(chunk * io.n_sub)), "r"(smem_u32(src))
                  : "memory");
-  } else if (io.mode == kIoBoxR) {
+  } else if (io_is<SET, kIoBoxR>(io)) {
     const int32_t img = (int32_t)(chunk / io.spi), cb = (int32_t)(chunk % io.spi);
     asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4}], [%5];" ::"l"(tm),
                  "r"(cb * io.C), "r"(0), "r"(0), "r"(img), "r"(smem_u32(src))
                  : "memory");
-  } else if (io.mode == kIoRank1) {
+  } else if (io_is<SET, kIoRank1>(io)) {
     const int32_t e0 = (int32_t)(chunk * io.chunk_rows);
     for (int i = 0; i < io.n_sub; ++i) tma_store_1d(tm, e0 + i * io.box_rows, src + i * io.sub_bytes);
-  } else if (io.mode == kIoFlat) {
+  } else if (io_is<SET, kIoFlat>(io)) {
     const int32_t row0 = (int32_t)(chunk * io.chunk_rows);
     for (int i = 0; i < io.n_sub; ++i) tma_store_2d(tm, 0, row0 + i * io.box_rows, src + i * io.sub_bytes);
   } else {
@@ -563,7 +584,7 @@ __global__ void __launch_bounds__(128 * NWG, MINB)
 #ifdef TCFFT_TRACE
     if (p.trace) p.trace[blockIdx.x * 8 + 1] = globaltimer_ns();
 #endif
-    if ((int64_t)blockIdx.x < p.chunks) issue_load(&tm_in, p.in, p.T, (int64_t)blockIdx.x, s_in, &bars[0]);
+    if ((int64_t)blockIdx.x < p.chunks) issue_load<IoSet<MODE>::IN>(&tm_in, p.in, p.T, (int64_t)blockIdx.x, s_in, &bars[0]);
   }
   // constants: B matrices, once per CTA
   for (int i = tid; i < p.bbytes / 16; i += NT)
@@ -685,7 +706,7 @@ __global__ void __launch_bounds__(128 * NWG, MINB)
         s_q[0] = nxt;  // read by all threads after this iteration's last barrier
         if (nxt < p.chunks) {
           // (single-buffer passes: issued after this chunk's store, below)
-          if constexpr (!ONEBUF) issue_load(&tm_in, p.in, p.T, nxt, s_in, &bars[0]);  // staging buffer is free again
+          if constexpr (!ONEBUF) issue_load<IoSet<MODE>::IN>(&tm_in, p.in, p.T, nxt, s_in, &bars[0]);  // staging buffer is free again
           if (p.ctr) s_q[1] = next_chunk(nxt);
         } else if (p.pdl == 1 && !triggered) {
           griddep_launch_dependents();  // this CTA's last chunk
@@ -844,12 +865,12 @@ __global__ void __launch_bounds__(128 * NWG, MINB)
       tc_fence_before();
       __syncthreads();
       if (tid == 0) {
-        issue_store<MODE == kModeStrip4>(&tm_out, p.out, p.T, chunk, s_a);
+        issue_store<IoSet<MODE>::OUT, MODE == kModeStrip4>(&tm_out, p.out, p.T, chunk, s_a);
         if constexpr (ONEBUF) {
           // the buffer is free once the store has read it: load the next chunk
           if (s_q[0] < p.chunks) {
             bulk_wait_read0();
-            issue_load(&tm_in, p.in, p.T, s_q[0], s_in, &bars[0]);
+            issue_load<IoSet<MODE>::IN>(&tm_in, p.in, p.T, s_q[0], s_in, &bars[0]);
           }
         }
       }
@@ -921,7 +942,7 @@ __global__ void __launch_bounds__(128 * NWG, MINB)
       tc_fence_after();
       const int64_t c1 = next_chunk(chunk0);
       s_q[1] = c1;  // read after the first writer barrier of iteration 0
-      if (c1 < p.chunks) issue_load(&tm_in, p.in, p.T, c1, s_in, &bars[0]);
+      if (c1 < p.chunks) issue_load<IoSet<MODE>::IN>(&tm_in, p.in, p.T, c1, s_in, &bars[0]);
       else if (p.pdl == 1 && !triggered) griddep_launch_dependents();
       issue_stage_mma<C, 0>(s_a_u, s_b_u, tD, tA);
       mma_commit(&bars[1]);
@@ -1020,14 +1041,14 @@ __global__ void __launch_bounds__(128 * NWG, MINB)
     __syncthreads();
     if (tid == 0) {
       tc_fence_after();
-      issue_store<MODE == kModeStrip4>(&tm_out, p.out, p.T, chunk, s_a);
+      issue_store<IoSet<MODE>::OUT, MODE == kModeStrip4>(&tm_out, p.out, p.T, chunk, s_a);
       if (has_next) {
         // next chunk: its staging buffer is free (gathered above): prefetch the
         // one after, start its stage-1 MMAs, then release the epilogue warps
         // once the store just issued has finished reading s_a
         const int64_t n2 = next_chunk(next);
         s_q[(it + 2) & 3] = n2;
-        if (n2 < p.chunks) issue_load(&tm_in, p.in, p.T, n2, s_in, &bars[0]);
+        if (n2 < p.chunks) issue_load<IoSet<MODE>::IN>(&tm_in, p.in, p.T, n2, s_in, &bars[0]);
         else if (p.pdl == 1 && !triggered) griddep_launch_dependents();
         issue_stage_mma<C, 0>(s_a_u, s_b_u, tD, tA);
         mma_commit(&bars[1]);
