@@ -357,13 +357,16 @@ DEVI void final_epilogue(uint32_t taddr, uint32_t s_out, int obase, int ostride,
 // I/O modes a kernel MODE can meet (plan.cpp build_pass / the exec paths):
 // the branches of the others compile out of thread 0's load / store issue,
 // which sits on every chunk's critical path (two extra runtime branches there
-// measured -5% on C3, profiles/exp_views2d_r02.txt)
+// measured -5% on C3, profiles/exp_views2d_r02.txt; these sets +2%,
+// profiles/exp_ioset_r02.txt)
 template <int MODE>
 struct IoSet {
   static constexpr uint32_t ROWS = (1u << kIoPitch) | (1u << kIoFlat) | (1u << kIoFlat3) | (1u << kIoRank1);
   static constexpr uint32_t BOXES = (1u << kIoBox) | (1u << kIoBoxR);
   static constexpr bool ROWK = MODE == kModeRow || MODE == kModeRowU;
-  static constexpr uint32_t IN = MODE == kModeRowTB ? (1u << kIoBlk) : (ROWK || MODE == kModeRowT) ? ROWS : ~0u;
+  // (column strips load boxes or flat tiles: never per-transform pitch copies or blocked rows)
+  static constexpr uint32_t STRIP_IN = ~((1u << kIoPitch) | (1u << kIoBlk));
+  static constexpr uint32_t IN = MODE == kModeRowTB ? (1u << kIoBlk) : (ROWK || MODE == kModeRowT) ? ROWS : STRIP_IN;
   static constexpr uint32_t OUT = (MODE == kModeRowTB || MODE == kModeRowT) ? BOXES : ROWK ? ROWS : ~0u;
 };
 // io.mode == M, decided at compile time when SET excludes M or holds only M
