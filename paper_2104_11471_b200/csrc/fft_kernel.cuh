@@ -359,7 +359,7 @@ DEVI void final_epilogue(uint32_t taddr, uint32_t s_out, int obase, int ostride,
 // which sits on every chunk's critical path (two extra runtime branches there
 // measured -5% on C3, profiles/exp_views2d_r02.txt; these sets +2%,
 // profiles/exp_ioset_r02.txt)
-template <int MODE>
+template <int MODE, bool TW4>
 struct IoSet {
   static constexpr uint32_t ROWS = (1u << kIoPitch) | (1u << kIoFlat) | (1u << kIoFlat3) | (1u << kIoRank1);
   static constexpr uint32_t BOXES = (1u << kIoBox) | (1u << kIoBoxR);
@@ -367,7 +367,15 @@ struct IoSet {
   // (column strips load boxes or flat tiles: never per-transform pitch copies or blocked rows)
   static constexpr uint32_t STRIP_IN = ~((1u << kIoPitch) | (1u << kIoBlk));
   static constexpr uint32_t IN = MODE == kModeRowTB ? (1u << kIoBlk) : (ROWK || MODE == kModeRowT) ? ROWS : STRIP_IN;
-  static constexpr uint32_t OUT = (MODE == kModeRowTB || MODE == kModeRowT) ? BOXES : ROWK ? ROWS : ~0u;
+  // stores: untwiddled column strips write where they read (2D columns), the
+  // 4D natural-order strips (three-step pass C, 2D split columns) one box;
+  // twiddled strips meet every store mode (contiguous / peer tiles, pitch rows)
+  static constexpr uint32_t OUT = (MODE == kModeRowTB || MODE == kModeRowT) ? BOXES
+                                  : ROWK                                   ? ROWS
+                                  : MODE == kModeStrip4                    ? (1u << kIoBox)
+                                  : (MODE == kModeStrip && !TW4)
+                                      ? BOXES | (1u << kIoFlat) | (1u << kIoFlat3) | (1u << kIoRank1)
+                                      : ~0u;
 };
 // io.mode == M, decided at compile time when SET excludes M or holds only M
 template <uint32_t SET, int M>
@@ -587,7 +595,7 @@ __global__ void __launch_bounds__(128 * NWG, MINB)
 #ifdef TCFFT_TRACE
     if (p.trace) p.trace[blockIdx.x * 8 + 1] = globaltimer_ns();
 #endif
-    if ((int64_t)blockIdx.x < p.chunks) issue_load<IoSet<MODE>::IN>(&tm_in, p.in, p.T, (int64_t)blockIdx.x, s_in, &bars[0]);
+    if ((int64_t)blockIdx.x < p.chunks) issue_load<IoSet<MODE, TW4>::IN>(&tm_in, p.in, p.T, (int64_t)blockIdx.x, s_in, &bars[0]);
   }
   // constants: B matrices, once per CTA
   for (int i = tid; i < p.bbytes / 16; i += NT)
@@ -709,7 +717,7 @@ __global__ void __launch_bounds__(128 * NWG, MINB)
         s_q[0] = nxt;  // read by all threads after this iteration's last barrier
         if (nxt < p.chunks) {
           // (single-buffer passes: issued after this chunk's store, below)
-          if constexpr (!ONEBUF) issue_load<IoSet<MODE>::IN>(&tm_in, p.in, p.T, nxt, s_in, &bars[0]);  // staging buffer is free again
+          if constexpr (!ONEBUF) issue_load<IoSet<MODE, TW4>::IN>(&tm_in, p.in, p.T, nxt, s_in, &bars[0]);  // staging buffer is free again
           if (p.ctr) s_q[1] = next_chunk(nxt);
         } else if (p.pdl == 1 && !triggered) {
           griddep_launch_dependents();  // this CTA's last chunk
@@ -868,12 +876,12 @@ __global__ void __launch_bounds__(128 * NWG, MINB)
       tc_fence_before();
       __syncthreads();
       if (tid == 0) {
-        issue_store<IoSet<MODE>::OUT, MODE == kModeStrip4>(&tm_out, p.out, p.T, chunk, s_a);
+        issue_store<IoSet<MODE, TW4>::OUT, MODE == kModeStrip4>(&tm_out, p.out, p.T, chunk, s_a);
         if constexpr (ONEBUF) {
           // the buffer is free once the store has read it: load the next chunk
           if (s_q[0] < p.chunks) {
             bulk_wait_read0();
-            issue_load<IoSet<MODE>::IN>(&tm_in, p.in, p.T, s_q[0], s_in, &bars[0]);
+            issue_load<IoSet<MODE, TW4>::IN>(&tm_in, p.in, p.T, s_q[0], s_in, &bars[0]);
           }
         }
       }
@@ -945,7 +953,7 @@ __global__ void __launch_bounds__(128 * NWG, MINB)
       tc_fence_after();
       const int64_t c1 = next_chunk(chunk0);
       s_q[1] = c1;  // read after the first writer barrier of iteration 0
-      if (c1 < p.chunks) issue_load<IoSet<MODE>::IN>(&tm_in, p.in, p.T, c1, s_in, &bars[0]);
+      if (c1 < p.chunks) issue_load<IoSet<MODE, TW4>::IN>(&tm_in, p.in, p.T, c1, s_in, &bars[0]);
       else if (p.pdl == 1 && !triggered) griddep_launch_dependents();
       issue_stage_mma<C, 0>(s_a_u, s_b_u, tD, tA);
       mma_commit(&bars[1]);
@@ -1044,14 +1052,14 @@ __global__ void __launch_bounds__(128 * NWG, MINB)
     __syncthreads();
     if (tid == 0) {
       tc_fence_after();
-      issue_store<IoSet<MODE>::OUT, MODE == kModeStrip4>(&tm_out, p.out, p.T, chunk, s_a);
+      issue_store<IoSet<MODE, TW4>::OUT, MODE == kModeStrip4>(&tm_out, p.out, p.T, chunk, s_a);
       if (has_next) {
         // next chunk: its staging buffer is free (gathered above): prefetch the
         // one after, start its stage-1 MMAs, then release the epilogue warps
         // once the store just issued has finished reading s_a
         const int64_t n2 = next_chunk(next);
         s_q[(it + 2) & 3] = n2;
-        if (n2 < p.chunks) issue_load<IoSet<MODE>::IN>(&tm_in, p.in, p.T, n2, s_in, &bars[0]);
+        if (n2 < p.chunks) issue_load<IoSet<MODE, TW4>::IN>(&tm_in, p.in, p.T, n2, s_in, &bars[0]);
         else if (p.pdl == 1 && !triggered) griddep_launch_dependents();
         issue_stage_mma<C, 0>(s_a_u, s_b_u, tD, tA);
         mma_commit(&bars[1]);
