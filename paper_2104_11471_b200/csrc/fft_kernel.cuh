@@ -385,6 +385,10 @@ DEVI bool io_is(const KIo& io) {
   else return io.mode == M;
 }
 
+// chunk ids fit 32 bits (< 2^32 chunks of >= 1024 elements): 32-bit instead of
+// 64-bit division on thread 0's per-chunk issue path
+DEVI uint32_t chunk32(int64_t c) { return (uint32_t)c; }
+
 template <uint32_t SET>
 DEVI void issue_load(const CUtensorMap* tm, const KIo& io, int T, int64_t chunk, uint8_t* dst, uint64_t* bar) {
   if (io_is<SET, kIoPitch>(io)) {
@@ -403,7 +407,7 @@ DEVI void issue_load(const CUtensorMap* tm, const KIo& io, int T, int64_t chunk,
         "l"(tm), "r"(0), "r"(0), "r"((int32_t)(chunk * io.n_sub)), "r"(smem_u32(bar))
         : "memory");
   } else if (io_is<SET, kIoBlk>(io)) {  // C-row group rb of every Bw-wide block of one image, 4D boxes of <= 256 blocks
-    const int32_t img = (int32_t)(chunk / io.spi), rb = (int32_t)(chunk % io.spi);
+    const int32_t img = (int32_t)(chunk32(chunk) / (uint32_t)io.spi), rb = (int32_t)(chunk32(chunk) % (uint32_t)io.spi);
     const int32_t bpb = io.box_rows;  // blocks per box
     for (int i = 0; i < io.n_sub; ++i)
       asm volatile(
@@ -412,7 +416,7 @@ DEVI void issue_load(const CUtensorMap* tm, const KIo& io, int T, int64_t chunk,
           "l"(tm), "r"(0), "r"(rb), "r"(i * bpb), "r"(img), "r"(smem_u32(bar))
           : "memory");
   } else if (io_is<SET, kIoBoxR>(io)) {  // whole > 256-row strip in one 4D box
-    const int32_t img = (int32_t)(chunk / io.spi), cb = (int32_t)(chunk % io.spi);
+    const int32_t img = (int32_t)(chunk32(chunk) / (uint32_t)io.spi), cb = (int32_t)(chunk32(chunk) % (uint32_t)io.spi);
     asm volatile(
         "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, "
         "%5}], [%6];" ::"r"(smem_u32(dst)),
@@ -425,7 +429,7 @@ DEVI void issue_load(const CUtensorMap* tm, const KIo& io, int T, int64_t chunk,
     const int32_t row0 = (int32_t)(chunk * io.chunk_rows);
     for (int i = 0; i < io.n_sub; ++i) tma_load_2d(dst + i * io.sub_bytes, tm, 0, row0 + i * io.box_rows, bar);
   } else {
-    const int32_t img = (int32_t)(chunk / io.spi), cb = (int32_t)(chunk % io.spi);
+    const int32_t img = (int32_t)(chunk32(chunk) / (uint32_t)io.spi), cb = (int32_t)(chunk32(chunk) % (uint32_t)io.spi);
     for (int i = 0; i < io.n_sub; ++i) {
         asm volatile(
             "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
@@ -457,7 +461,7 @@ DEVI void issue_store(const CUtensorMap* tm, const KIo& io, int T, int64_t chunk
                  "r"(0), "r"(0), "r"((int32_t)(chunk * io.n_sub)), "r"(smem_u32(src))
                  : "memory");
   } else if (io_is<SET, kIoBoxR>(io)) {
-    const int32_t img = (int32_t)(chunk / io.spi), cb = (int32_t)(chunk % io.spi);
+    const int32_t img = (int32_t)(chunk32(chunk) / (uint32_t)io.spi), cb = (int32_t)(chunk32(chunk) % (uint32_t)io.spi);
     asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4}], [%5];" ::"l"(tm),
                  "r"(cb * io.C), "r"(0), "r"(0), "r"(img), "r"(smem_u32(src))
                  : "memory");
@@ -468,7 +472,7 @@ DEVI void issue_store(const CUtensorMap* tm, const KIo& io, int T, int64_t chunk
     const int32_t row0 = (int32_t)(chunk * io.chunk_rows);
     for (int i = 0; i < io.n_sub; ++i) tma_store_2d(tm, 0, row0 + i * io.box_rows, src + i * io.sub_bytes);
   } else {
-    const int32_t img = (int32_t)(chunk / io.spi), cb = (int32_t)(chunk % io.spi);
+    const int32_t img = (int32_t)(chunk32(chunk) / (uint32_t)io.spi), cb = (int32_t)(chunk32(chunk) % (uint32_t)io.spi);
     for (int i = 0; i < io.n_sub; ++i) {
       if constexpr (D4)
         asm volatile(
